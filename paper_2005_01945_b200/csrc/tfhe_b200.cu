@@ -1,0 +1,547 @@
+// libtfhe_b200.so -- sm_100a kernels and the C ABI declared in include/tfhe_b200.h.
+//
+// Kernels
+//   K1 k_gate_bootstrap   fused gate linear form + mod switch + n-step CMux blind
+//                         rotation + sample extract; one ciphertext per 64-thread
+//                         group, ACC resident in shared memory, FP64 negacyclic FFT
+//                         in registers (tfhe_device.cuh)
+//   K2 k_key_switch       batched N -> n key switch as an integer rank-8192 update,
+//                         32 ciphertexts x 512 columns per CTA, digits in smem
+//   K3 k_bk_transform     one-time: raw TRGSW rows -> spectral key in K1's register
+//      k_ksk_layout       order; raw key-switching key -> row-padded table
+//   k_rows_negate, k_rows_phase   NOT and batched phase (decryption helper)
+//   k_peak_*              DFMA / IMAD peak microbenchmarks (roofline denominators)
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/tfhe_b200.h"
+#include "tfhe_device.cuh"
+
+using namespace tfb;
+
+static_assert(TFB_ROW_STRIDE == ROW_STRIDE, "header / device stride mismatch");
+static_assert(TFB_EXT_STRIDE == EXT_STRIDE, "header / device stride mismatch");
+
+// ------------------------------------------------------------------------------------
+// context
+// ------------------------------------------------------------------------------------
+struct tfb_ctx {
+  int device = 0;
+  tfb_params p{};
+  bool keys_loaded = false;
+  cd* d_bkf = nullptr;         // [n][4][8][2][64] cd, prescaled by 1/512
+  int32_t* d_ksk = nullptr;    // [N*t][ROW_STRIDE]
+  Twiddles* d_tw = nullptr;
+  uint32_t* d_ext = nullptr;   // scratch [cap][EXT_STRIDE]
+  int64_t ext_cap = 0;
+  // buffers of the host-buffer launch path
+  uint32_t* d_hx = nullptr;    // [cap][ROW_STRIDE] x, y, out back to back
+  uint8_t* d_hkinds = nullptr;
+  int32_t* d_hrows = nullptr;  // identity row indices
+  int64_t host_cap = 0;
+  int64_t launches = 0;
+  std::string err;
+};
+
+static thread_local std::string g_create_err;
+
+#define TFB_CUDA(ctx, call)                                                            \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(e_);                 \
+      return TFB_ERR_CUDA;                                                             \
+    }                                                                                  \
+  } while (0)
+
+struct BlockSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct LdgBk {
+  __device__ __forceinline__ cd operator()(const cd* p) const {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    return cd{v.x, v.y};
+  }
+};
+
+// ------------------------------------------------------------------------------------
+// K1: fused gate bootstrap (one ciphertext per 64-thread CTA)
+// ------------------------------------------------------------------------------------
+constexpr int K1_SMEM_FIXED = 2 * HALF_N * (int)sizeof(cd) + 2 * RING_N * (int)sizeof(uint32_t);
+
+__global__ void __launch_bounds__(FFT_THREADS) k_gate_bootstrap(
+    const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
+    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
+    const cd* __restrict__ bkf, const Twiddles* __restrict__ tw, uint32_t* __restrict__ ext) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  cd* bufA = reinterpret_cast<cd*>(smem);
+  cd* bufB = bufA + HALF_N;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(bufB + HALF_N);
+  uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
+  const int64_t g = blockIdx.x;
+  const uint32_t* xr = pool + (int64_t)x_rows[g] * ROW_STRIDE;
+  const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
+  BlockSync sync;
+  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bkf, tw, acc, abar, bufA, bufB, ext + g * EXT_STRIDE,
+                 (int)threadIdx.x, sync, LdgBk());
+}
+
+// ------------------------------------------------------------------------------------
+// K2: key switch.  out[c][col] = (col == n ? ext_b[c] : 0) - sum_r digit[c][r] * ksk[r][col]
+//     r = i*KS_T + j over the N*KS_T digit rows; CTA tile = KS_CT ciphertexts x 512 columns.
+// ------------------------------------------------------------------------------------
+constexpr int KS_CT = 32;        // ciphertexts per CTA
+constexpr int KS_THREADS = 256;  // 2 columns per thread
+constexpr int KS_CHUNK_I = 16;   // ring coefficients per digit chunk
+constexpr int KS_CHUNK_R = KS_CHUNK_I * KS_T;
+
+__global__ void __launch_bounds__(KS_THREADS) k_key_switch(const uint32_t* __restrict__ ext,
+                                                           const int32_t* __restrict__ ksk,
+                                                           uint32_t* __restrict__ pool,
+                                                           const int32_t* __restrict__ out_rows, int n,
+                                                           int64_t k) {
+  __shared__ __align__(16) int32_t digits[KS_CHUNK_R][KS_CT];
+  const int tid = threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.x * KS_CT;
+  int32_t acc0[KS_CT], acc1[KS_CT];
+#pragma unroll
+  for (int c = 0; c < KS_CT; ++c) acc0[c] = acc1[c] = 0;
+  const uint32_t bias = ks_bias();
+
+  for (int i0 = 0; i0 < RING_N; i0 += KS_CHUNK_I) {
+    __syncthreads();
+    // digits of ext[c][i0 .. i0+16) for the tile's ciphertexts: 512 words, 2 per thread
+    for (int e = tid; e < KS_CT * KS_CHUNK_I; e += KS_THREADS) {
+      const int c = e / KS_CHUNK_I, ii = e % KS_CHUNK_I;
+      uint32_t a = 0;
+      if (c0 + c < k) a = ext[(c0 + c) * EXT_STRIDE + i0 + ii];
+      const uint32_t ab = a + bias;
+      const bool live = (c0 + c < k);
+#pragma unroll
+      for (int j = 0; j < KS_T; ++j) digits[ii * KS_T + j][c] = live ? ks_digit(ab, j) : 0;
+    }
+    __syncthreads();
+    const int32_t* kr = ksk + (int64_t)i0 * KS_T * ROW_STRIDE;
+#pragma unroll 4
+    for (int r = 0; r < KS_CHUNK_R; ++r) {
+      const int32_t k0 = __ldg(kr + (int64_t)r * ROW_STRIDE + tid);
+      const int32_t k1 = __ldg(kr + (int64_t)r * ROW_STRIDE + tid + KS_THREADS);
+      const int4* d4 = reinterpret_cast<const int4*>(&digits[r][0]);
+#pragma unroll
+      for (int q = 0; q < KS_CT / 4; ++q) {
+        const int4 d = d4[q];
+        acc0[4 * q + 0] += d.x * k0;
+        acc1[4 * q + 0] += d.x * k1;
+        acc0[4 * q + 1] += d.y * k0;
+        acc1[4 * q + 1] += d.y * k1;
+        acc0[4 * q + 2] += d.z * k0;
+        acc1[4 * q + 2] += d.z * k1;
+        acc0[4 * q + 3] += d.w * k0;
+        acc1[4 * q + 3] += d.w * k1;
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < KS_CT; ++c) {
+    if (c0 + c >= k) break;
+    uint32_t* row = pool + (int64_t)out_rows[c0 + c] * ROW_STRIDE;
+    const uint32_t body = ext[(c0 + c) * EXT_STRIDE + RING_N];
+    row[tid] = (tid == n ? body : 0u) - (uint32_t)acc0[c];
+    row[tid + KS_THREADS] = (tid + KS_THREADS == n ? body : 0u) - (uint32_t)acc1[c];
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K3: key setup
+// ------------------------------------------------------------------------------------
+// one CTA per raw polynomial: bk_raw[(i*4 + r)*2 + c][N] -> bkf[i][r][k2][c][t]
+__global__ void __launch_bounds__(FFT_THREADS) k_bk_transform(const int32_t* __restrict__ bk_raw,
+                                                              cd* __restrict__ bkf,
+                                                              const Twiddles* __restrict__ tw) {
+  __shared__ cd bufA[HALF_N];
+  __shared__ cd bufB[HALF_N];
+  const int t = threadIdx.x;
+  const int64_t poly = blockIdx.x;
+  const int c = (int)(poly & 1);
+  const int64_t ir = poly >> 1;  // i*4 + r
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(bk_raw) + poly * RING_N;
+  cd x[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m)
+    x[m] = cd{int32_to_double(src[t + 64 * m]), int32_to_double(src[t + 64 * m + HALF_N])};
+  BlockSync sync;
+  fft_forward(x, t, tw, bufA, bufB, sync);
+  const double scale = 1.0 / HALF_N;
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2)
+    bkf[((ir * 8 + k2) * 2 + c) * FFT_THREADS + t] = cd{x[k2].re * scale, x[k2].im * scale};
+}
+
+// ksk_raw[N*t][n+1] -> ksk[N*t][ROW_STRIDE], zero padded
+__global__ void k_ksk_layout(const int32_t* __restrict__ raw, int32_t* __restrict__ out, int n) {
+  const int64_t r = blockIdx.x;
+  for (int c = threadIdx.x; c < ROW_STRIDE; c += blockDim.x)
+    out[r * ROW_STRIDE + c] = (c <= n) ? raw[r * (n + 1) + c] : 0;
+}
+
+// ------------------------------------------------------------------------------------
+// small row kernels
+// ------------------------------------------------------------------------------------
+__global__ void k_rows_negate(uint32_t* __restrict__ pool, const int32_t* __restrict__ in_rows,
+                              const int32_t* __restrict__ out_rows) {
+  const uint32_t* src = pool + (int64_t)in_rows[blockIdx.x] * ROW_STRIDE;
+  uint32_t* dst = pool + (int64_t)out_rows[blockIdx.x] * ROW_STRIDE;
+  for (int c = threadIdx.x; c < ROW_STRIDE; c += blockDim.x) dst[c] = 0u - src[c];
+}
+
+__global__ void k_rows_phase(const uint32_t* __restrict__ pool, const int32_t* __restrict__ rows,
+                             const uint32_t* __restrict__ key_bits, uint32_t* __restrict__ phase, int n) {
+  const uint32_t* row = pool + (int64_t)rows[blockIdx.x] * ROW_STRIDE;
+  uint32_t s = 0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) s += row[c] * key_bits[c];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  __shared__ uint32_t part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += part[w];
+    phase[blockIdx.x] = row[n] - tot;
+  }
+}
+
+// packed host layout [k][n+1] <-> pool rows, used by the host-buffer launch
+__global__ void k_identity_rows(int32_t* rows, int64_t count, int32_t base) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) rows[i] = base + (int32_t)i;
+}
+
+// ------------------------------------------------------------------------------------
+// peak microbenchmarks
+// ------------------------------------------------------------------------------------
+__global__ void k_peak_dfma(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+         a7 = a0 + 7;
+  const double m = 1.0000001, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+__global__ void k_peak_imad(int32_t* out, int iters) {
+  int32_t a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+          a7 = a0 + 7;
+  const int32_t m = (int32_t)blockIdx.x | 3, c = 12345;
+  for (int i = 0; i < iters; ++i) {
+    a0 = a0 * m + c; a1 = a1 * m + c; a2 = a2 * m + c; a3 = a3 * m + c;
+    a4 = a4 * m + c; a5 = a5 * m + c; a6 = a6 * m + c; a7 = a7 * m + c;
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+
+// ------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------
+static void fill_twiddles(Twiddles* tw) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int k = 0; k < 8; ++k)
+    for (int t = 0; t < FFT_THREADS; ++t) {
+      const long double ang = pi * (long double)(t * (1 + 4 * k)) / (long double)RING_N;
+      tw->tw1[k][t] = cd{(double)cosl(ang), (double)sinl(ang)};
+    }
+  for (int k = 0; k < 8; ++k)
+    for (int a = 0; a < 8; ++a) {
+      const long double ang = 2.0L * pi * (long double)(a * k) / 64.0L;
+      tw->tw2[k][a] = cd{(double)cosl(ang), (double)sinl(ang)};
+    }
+}
+
+static int ensure_ext(tfb_ctx* ctx, int64_t k) {
+  if (k <= ctx->ext_cap) return TFB_OK;
+  if (ctx->d_ext) TFB_CUDA(ctx, cudaFree(ctx->d_ext));
+  ctx->d_ext = nullptr;
+  ctx->ext_cap = 0;
+  int64_t cap = 1024;
+  while (cap < k) cap *= 2;
+  TFB_CUDA(ctx, cudaMalloc(&ctx->d_ext, (size_t)cap * EXT_STRIDE * sizeof(uint32_t)));
+  ctx->ext_cap = cap;
+  return TFB_OK;
+}
+
+extern "C" {
+
+int tfb_abi_version(void) { return TFB_ABI_VERSION; }
+
+const char* tfb_last_error(const tfb_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
+  if (!p || !out) {
+    g_create_err = "null argument";
+    return TFB_ERR_INVALID;
+  }
+  if (p->ring_n != RING_N || p->bk_l != BK_L || p->bk_bgbit != BK_BGBIT || p->ks_t != KS_T ||
+      p->ks_basebit != KS_BASEBIT || p->n < 1 || p->n >= ROW_STRIDE) {
+    g_create_err = "unsupported parameter set (compiled: N=1024 l=2 Bgbit=10 t=8 basebit=2, n<=511)";
+    return TFB_ERR_INVALID;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    g_create_err = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+    return TFB_ERR_CUDA;
+  }
+  tfb_ctx* ctx = new tfb_ctx();
+  ctx->device = device;
+  ctx->p = *p;
+  Twiddles* h = new Twiddles();
+  fill_twiddles(h);
+  e = cudaMalloc(&ctx->d_tw, sizeof(Twiddles));
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw, h, sizeof(Twiddles), cudaMemcpyHostToDevice);
+  delete h;
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gate_bootstrap, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  if (e != cudaSuccess) {
+    g_create_err = std::string("context setup: ") + cudaGetErrorString(e);
+    delete ctx;
+    return TFB_ERR_CUDA;
+  }
+  *out = ctx;
+  return TFB_OK;
+}
+
+void tfb_ctx_destroy(tfb_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaFree(ctx->d_bkf);
+  cudaFree(ctx->d_ksk);
+  cudaFree(ctx->d_tw);
+  cudaFree(ctx->d_ext);
+  cudaFree(ctx->d_hx);
+  cudaFree(ctx->d_hkinds);
+  cudaFree(ctx->d_hrows);
+  delete ctx;
+}
+
+int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_device, void* stream) {
+  if (!ctx || !bk || !ksk) return TFB_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int n = ctx->p.n;
+  const size_t bk_words = (size_t)n * BK_ROWS * 2 * RING_N;
+  const size_t ksk_words = (size_t)RING_N * KS_T * (n + 1);
+  const int32_t* d_bk = bk;
+  const int32_t* d_kr = ksk;
+  int32_t *tmp_bk = nullptr, *tmp_ksk = nullptr;
+  if (!on_device) {
+    TFB_CUDA(ctx, cudaMalloc(&tmp_bk, bk_words * 4));
+    TFB_CUDA(ctx, cudaMalloc(&tmp_ksk, ksk_words * 4));
+    TFB_CUDA(ctx, cudaMemcpyAsync(tmp_bk, bk, bk_words * 4, cudaMemcpyHostToDevice, st));
+    TFB_CUDA(ctx, cudaMemcpyAsync(tmp_ksk, ksk, ksk_words * 4, cudaMemcpyHostToDevice, st));
+    d_bk = tmp_bk;
+    d_kr = tmp_ksk;
+  }
+  if (!ctx->d_bkf) TFB_CUDA(ctx, cudaMalloc(&ctx->d_bkf, (size_t)n * BK_ROWS * 2 * HALF_N * sizeof(cd)));
+  if (!ctx->d_ksk) TFB_CUDA(ctx, cudaMalloc(&ctx->d_ksk, (size_t)RING_N * KS_T * ROW_STRIDE * 4));
+  k_bk_transform<<<n * BK_ROWS * 2, FFT_THREADS, 0, st>>>(d_bk, ctx->d_bkf, ctx->d_tw);
+  k_ksk_layout<<<RING_N * KS_T, 128, 0, st>>>(d_kr, ctx->d_ksk, n);
+  ctx->launches += 2;
+  TFB_CUDA(ctx, cudaGetLastError());
+  TFB_CUDA(ctx, cudaStreamSynchronize(st));
+  if (tmp_bk) cudaFree(tmp_bk);
+  if (tmp_ksk) cudaFree(tmp_ksk);
+  ctx->keys_loaded = true;
+  return TFB_OK;
+}
+
+static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds, const int32_t* xr,
+                               const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
+  const int smem = K1_SMEM_FIXED + ((ctx->p.n + 1) * 2 + 15) / 16 * 16;
+  k_gate_bootstrap<<<(unsigned)k, FFT_THREADS, smem, st>>>((const uint32_t*)pool, kinds, xr, yr, ctx->p.n,
+                                                           ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
+  ctx->launches += 1;
+  TFB_CUDA(ctx, cudaGetLastError());
+  return TFB_OK;
+}
+
+static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, const int32_t* out_rows,
+                             int64_t k, cudaStream_t st) {
+  const unsigned grid = (unsigned)((k + KS_CT - 1) / KS_CT);
+  k_key_switch<<<grid, KS_THREADS, 0, st>>>(ext, ctx->d_ksk, (uint32_t*)pool, out_rows, ctx->p.n, k);
+  ctx->launches += 1;
+  TFB_CUDA(ctx, cudaGetLastError());
+  return TFB_OK;
+}
+
+static int check_launch_args(tfb_ctx* ctx, int64_t k) {
+  if (!ctx) return TFB_ERR_INVALID;
+  if (!ctx->keys_loaded) {
+    ctx->err = "keys not loaded";
+    return TFB_ERR_STATE;
+  }
+  if (k < 1 || k > (int64_t)0x7fffffff) {
+    ctx->err = "k out of range";
+    return TFB_ERR_INVALID;
+  }
+  return TFB_OK;
+}
+
+int tfb_gate_launch(tfb_ctx* ctx, void* pool, const uint8_t* kinds, const int32_t* xr, const int32_t* yr,
+                    const int32_t* out_rows, int64_t k, void* stream) {
+  int rc = check_launch_args(ctx, k);
+  if (rc) return rc;
+  if (!pool || !kinds || !xr || !yr || !out_rows) return TFB_ERR_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  if ((rc = ensure_ext(ctx, k))) return rc;
+  if ((rc = launch_blind_rotate(ctx, pool, kinds, xr, yr, ctx->d_ext, k, st))) return rc;
+  return launch_key_switch(ctx, ctx->d_ext, pool, out_rows, k, st);
+}
+
+int tfb_debug_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds, const int32_t* xr,
+                           const int32_t* yr, uint32_t* ext, int64_t k, void* stream) {
+  int rc = check_launch_args(ctx, k);
+  if (rc) return rc;
+  if (!pool || !kinds || !xr || !yr || !ext) return TFB_ERR_INVALID;
+  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  return launch_blind_rotate(ctx, pool, kinds, xr, yr, ext, k, (cudaStream_t)stream);
+}
+
+int tfb_debug_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, const int32_t* out_rows, int64_t k,
+                         void* stream) {
+  int rc = check_launch_args(ctx, k);
+  if (rc) return rc;
+  if (!pool || !ext || !out_rows) return TFB_ERR_INVALID;
+  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  return launch_key_switch(ctx, ext, pool, out_rows, k, (cudaStream_t)stream);
+}
+
+int tfb_gate_launch_host(tfb_ctx* ctx, const uint32_t* x, const uint32_t* y, const uint8_t* kinds,
+                         uint32_t* out, int64_t k) {
+  int rc = check_launch_args(ctx, k);
+  if (rc) return rc;
+  if (!x || !y || !kinds || !out) return TFB_ERR_INVALID;
+  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  if (k > ctx->host_cap) {
+    cudaFree(ctx->d_hx);
+    cudaFree(ctx->d_hkinds);
+    cudaFree(ctx->d_hrows);
+    ctx->d_hx = nullptr;
+    ctx->d_hkinds = nullptr;
+    ctx->d_hrows = nullptr;
+    ctx->host_cap = 0;
+    int64_t cap = 256;
+    while (cap < k) cap *= 2;
+    TFB_CUDA(ctx, cudaMalloc(&ctx->d_hx, (size_t)3 * cap * ROW_STRIDE * 4));
+    TFB_CUDA(ctx, cudaMalloc(&ctx->d_hkinds, (size_t)cap));
+    TFB_CUDA(ctx, cudaMalloc(&ctx->d_hrows, (size_t)3 * cap * 4));
+    k_identity_rows<<<(unsigned)((3 * cap + 255) / 256), 256>>>(ctx->d_hrows, 3 * cap, 0);
+    ctx->launches += 1;
+    TFB_CUDA(ctx, cudaGetLastError());
+    ctx->host_cap = cap;
+  }
+  const int64_t cap = ctx->host_cap;
+  const size_t wpitch = (size_t)(ctx->p.n + 1) * 4, dpitch = (size_t)ROW_STRIDE * 4;
+  uint32_t* dx = ctx->d_hx;
+  uint32_t* dy = ctx->d_hx + (size_t)cap * ROW_STRIDE;
+  uint32_t* dout = ctx->d_hx + (size_t)2 * cap * ROW_STRIDE;
+  cudaStream_t st = 0;
+  TFB_CUDA(ctx, cudaMemcpy2DAsync(dx, dpitch, x, wpitch, wpitch, (size_t)k, cudaMemcpyHostToDevice, st));
+  TFB_CUDA(ctx, cudaMemcpy2DAsync(dy, dpitch, y, wpitch, wpitch, (size_t)k, cudaMemcpyHostToDevice, st));
+  TFB_CUDA(ctx, cudaMemcpyAsync(ctx->d_hkinds, kinds, (size_t)k, cudaMemcpyHostToDevice, st));
+  if ((rc = ensure_ext(ctx, k))) return rc;
+  // rows: x = [0,cap), y = [cap, 2cap), out = [2cap, 3cap) of the d_hx pool
+  if ((rc = launch_blind_rotate(ctx, ctx->d_hx, ctx->d_hkinds, ctx->d_hrows, ctx->d_hrows + cap, ctx->d_ext, k,
+                                st)))
+    return rc;
+  if ((rc = launch_key_switch(ctx, ctx->d_ext, ctx->d_hx, ctx->d_hrows + 2 * cap, k, st))) return rc;
+  TFB_CUDA(ctx, cudaMemcpy2DAsync(out, wpitch, dout, dpitch, wpitch, (size_t)k, cudaMemcpyDeviceToHost, st));
+  TFB_CUDA(ctx, cudaStreamSynchronize(st));
+  return TFB_OK;
+}
+
+int tfb_rows_negate(tfb_ctx* ctx, void* pool, const int32_t* in_rows, const int32_t* out_rows, int64_t k,
+                    void* stream) {
+  if (!ctx || !pool || !in_rows || !out_rows || k < 1) return TFB_ERR_INVALID;
+  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  k_rows_negate<<<(unsigned)k, 128, 0, (cudaStream_t)stream>>>((uint32_t*)pool, in_rows, out_rows);
+  ctx->launches += 1;
+  TFB_CUDA(ctx, cudaGetLastError());
+  return TFB_OK;
+}
+
+int tfb_rows_phase(tfb_ctx* ctx, const void* pool, const int32_t* rows, const uint32_t* key_bits,
+                   uint32_t* phase, int64_t k, void* stream) {
+  if (!ctx || !pool || !rows || !key_bits || !phase || k < 1) return TFB_ERR_INVALID;
+  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  k_rows_phase<<<(unsigned)k, 128, 0, (cudaStream_t)stream>>>((const uint32_t*)pool, rows, key_bits, phase,
+                                                             ctx->p.n);
+  ctx->launches += 1;
+  TFB_CUDA(ctx, cudaGetLastError());
+  return TFB_OK;
+}
+
+int tfb_debug_spectral_key(tfb_ctx* ctx, int32_t i, double* out) {
+  if (!ctx || !out || i < 0 || i >= ctx->p.n) return TFB_ERR_INVALID;
+  if (!ctx->keys_loaded) return TFB_ERR_STATE;
+  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  const size_t per_i = (size_t)BK_ROWS * 8 * 2 * FFT_THREADS;
+  std::vector<cd> h(per_i);
+  TFB_CUDA(ctx, cudaMemcpy(h.data(), ctx->d_bkf + (size_t)i * per_i, per_i * sizeof(cd), cudaMemcpyDeviceToHost));
+  for (int r = 0; r < BK_ROWS; ++r)
+    for (int k2 = 0; k2 < 8; ++k2)
+      for (int c = 0; c < 2; ++c)
+        for (int t = 0; t < FFT_THREADS; ++t) {
+          const cd v = h[((size_t)(r * 8 + k2) * 2 + c) * FFT_THREADS + t];
+          const int f = spectral_index(t, k2);
+          double* dst = out + (((size_t)(r * 2 + c) * HALF_N) + f) * 2;
+          dst[0] = v.re * HALF_N;
+          dst[1] = v.im * HALF_N;
+        }
+  return TFB_OK;
+}
+
+int64_t tfb_kernel_launches(const tfb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int tfb_measure_peaks(int device, double* fp64_tflops, double* int32_tops) {
+  if (cudaSetDevice(device) != cudaSuccess) return TFB_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return TFB_ERR_CUDA;
+  const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 1 << 16;
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, (size_t)blocks * threads * 8) != cudaSuccess) return TFB_ERR_CUDA;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms = 0;
+  double best_d = 0, best_i = 0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0);
+    k_peak_dfma<<<blocks, threads>>>((double*)buf, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double tf = 2.0 * 8.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
+    if (rep && tf > best_d) best_d = tf;
+    cudaEventRecord(e0);
+    k_peak_imad<<<blocks, threads>>>((int32_t*)buf, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double to = 8.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
+    if (rep && to > best_i) best_i = to;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  if (cudaGetLastError() != cudaSuccess) return TFB_ERR_CUDA;
+  if (fp64_tflops) *fp64_tflops = best_d;
+  if (int32_tops) *int32_tops = best_i;
+  return TFB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,339 @@
+// Per-thread building blocks of the B200 gate-bootstrapping kernels.
+//
+// Everything in this header is written as `__host__ __device__` code with the
+// barrier abstracted behind a `Sync` functor, so the exact arithmetic the
+// sm_100a kernels execute can also be driven by 64 host threads + a pthread
+// barrier (tests/emu) on a box without a GPU.  The kernels themselves live in
+// tfhe_b200.cu.
+//
+// Algorithm (TFHE gate bootstrapping, CGGI16/17; the reference replaces it
+// with a key-holding oracle at encirc/engine.py:493-503, so there is no
+// reference code to follow here -- see DESIGN.md "parity unpinned"):
+//
+//   gate linear form  (a', b') = cx*x + cy*y + off*mu        encirc/engine.py:483-484
+//   mod switch        abar_i = round(a'_i * 2N / 2^32)
+//   ACC <- (0, X^{2N-bbar} * (mu + mu X + ... + mu X^{N-1}))
+//   for i < n:        ACC <- ACC + BK_i [.] ((X^{abar_i} - 1) * ACC)     (CMux)
+//   sample extract    coefficient 0 of ACC -> LWE sample of dimension N
+//   key switch        N -> n with signed base-4 digits
+//
+// The external product is evaluated with a negacyclic FP64 FFT: a polynomial
+// of N = 1024 real coefficients is folded to 512 complex points, twisted by
+// exp(i pi j / N) and transformed by a 512-point complex FFT done as three
+// radix-8 passes, 8 points per thread, 64 threads per polynomial, with two
+// shared-memory exchanges per transform.  With Bg = 2^10, l = 2 the exact
+// integer result is below 2^52 and the observed FFT error is ~0.01 (std) on a
+// rounding threshold of 0.5, so the rounded result equals the exact integer
+// product; the parity tests hold the kernel to bit-exact agreement with the
+// integer oracle.
+#pragma once
+#include <stdint.h>
+#include <string.h>
+
+#if defined(__CUDACC__)
+#define TFB_HD __host__ __device__ __forceinline__
+#else
+#define TFB_HD inline
+#endif
+
+namespace tfb {
+
+// ---- fixed ring-side parameter set (checked at tfb_ctx_create) -------------
+constexpr int RING_N = 1024;          // TRLWE degree
+constexpr int HALF_N = RING_N / 2;    // complex points per transform
+constexpr int BK_L = 2;               // gadget length
+constexpr int BK_BGBIT = 10;          // log2 gadget base
+constexpr int BK_ROWS = 2 * BK_L;     // (k+1)*l TRLWE rows per TRGSW
+constexpr int KS_T = 8;               // key-switch digits
+constexpr int KS_BASEBIT = 2;         // log2 key-switch base
+constexpr int FFT_THREADS = 64;       // threads per polynomial transform
+constexpr int ROW_STRIDE = 512;       // int32 words per pool row (n+1 <= 512)
+constexpr int EXT_STRIDE = RING_N + 8;  // words per extracted sample (N+1, padded)
+
+constexpr uint32_t DECOMP_OFFSET =
+    (uint32_t(1) << 31) + (uint32_t(1) << (31 - BK_BGBIT));  // sum_l Bg/2 * 2^(32-(l+1)*bgbit)
+
+struct alignas(16) cd {
+  double re, im;
+};
+
+TFB_HD cd cmul(cd a, cd b) { return cd{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+TFB_HD cd cmulc(cd a, cd b) {  // a * conj(b)
+  return cd{a.re * b.re + a.im * b.im, a.im * b.re - a.re * b.im};
+}
+TFB_HD cd cadd(cd a, cd b) { return cd{a.re + b.re, a.im + b.im}; }
+TFB_HD cd csub(cd a, cd b) { return cd{a.re - b.re, a.im - b.im}; }
+TFB_HD void cmac(cd& acc, cd a, cd b) {
+  acc.re += a.re * b.re - a.im * b.im;
+  acc.im += a.re * b.im + a.im * b.re;
+}
+
+TFB_HD double bits_to_double(uint64_t u) {
+#if defined(__CUDA_ARCH__)
+  return __longlong_as_double((long long)u);
+#else
+  double d;
+  memcpy(&d, &u, 8);
+  return d;
+#endif
+}
+TFB_HD uint64_t double_to_bits(double d) {
+#if defined(__CUDA_ARCH__)
+  return (uint64_t)__double_as_longlong(d);
+#else
+  uint64_t u;
+  memcpy(&u, &d, 8);
+  return u;
+#endif
+}
+
+// 10-bit unsigned digit field -> exact double of the signed digit field-512.
+// (2^52 + field) has `field` in its low mantissa bits; one subtraction undoes
+// the bias.  Avoids the slow I2F.F64 conversion pipe.
+TFB_HD double digit_to_double(uint32_t field) {
+  return bits_to_double(0x4330000000000000ull | (uint64_t)field) - (4503599627370496.0 + 512.0);
+}
+// int32 (as uint32 bit pattern) -> exact double
+TFB_HD double int32_to_double(uint32_t v) {
+  return bits_to_double(0x4330000000000000ull | (uint64_t)(v ^ 0x80000000u)) -
+         (4503599627370496.0 + 2147483648.0);
+}
+// round-to-nearest-even(x) mod 2^32, valid for |x| < 2^51
+TFB_HD uint32_t round_to_word(double x) {
+  return (uint32_t)double_to_bits(x + 6755399441055744.0);
+}
+
+// ---- 8-point DFT in registers ----------------------------------------------
+// X[k] = sum_m x[m] * exp(SIGN * 2 pi i m k / 8), natural order in and out.
+template <int SIGN>
+TFB_HD cd mul_i(cd a) {  // a * (SIGN * i)
+  return SIGN > 0 ? cd{-a.im, a.re} : cd{a.im, -a.re};
+}
+
+template <int SIGN>
+TFB_HD void dft8(cd* x) {
+  const double h = 0.70710678118654752440;
+  cd a0 = cadd(x[0], x[4]), a1 = cadd(x[1], x[5]), a2 = cadd(x[2], x[6]), a3 = cadd(x[3], x[7]);
+  cd b0 = csub(x[0], x[4]), b1 = csub(x[1], x[5]), b2 = csub(x[2], x[6]), b3 = csub(x[3], x[7]);
+  // b_m *= W8^(SIGN*m)
+  {
+    cd t = b1;  // (1 + SIGN i)/sqrt2
+    b1 = SIGN > 0 ? cd{(t.re - t.im) * h, (t.re + t.im) * h} : cd{(t.re + t.im) * h, (t.im - t.re) * h};
+    b2 = mul_i<SIGN>(b2);
+    t = b3;  // (-1 + SIGN i)/sqrt2
+    b3 = SIGN > 0 ? cd{(-t.re - t.im) * h, (t.re - t.im) * h} : cd{(t.im - t.re) * h, (-t.re - t.im) * h};
+  }
+  // two 4-point DFTs
+  cd c0 = cadd(a0, a2), c1 = cadd(a1, a3), d0 = csub(a0, a2), d1 = mul_i<SIGN>(csub(a1, a3));
+  x[0] = cadd(c0, c1);
+  x[4] = csub(c0, c1);
+  x[2] = cadd(d0, d1);
+  x[6] = csub(d0, d1);
+  c0 = cadd(b0, b2), c1 = cadd(b1, b3), d0 = csub(b0, b2), d1 = mul_i<SIGN>(csub(b1, b3));
+  x[1] = cadd(c0, c1);
+  x[5] = csub(c0, c1);
+  x[3] = cadd(d0, d1);
+  x[7] = csub(d0, d1);
+}
+
+// ---- twiddle tables ----------------------------------------------------------
+// tw1[k][t]   = exp(i pi t (1 + 4k) / 1024)   (pass-1 twiddle W512^{t k} with the
+//               per-thread part exp(i pi t / N) of the negacyclic twist folded in)
+// tw2[k][a]   = exp(2 pi i a k / 64)          (pass-2 twiddle)
+// Both are stored [register index][thread] so a warp reads consecutive words.
+struct Twiddles {
+  cd tw1[8][FFT_THREADS];
+  cd tw2[8][8];
+};
+
+// exp(i pi m / 16): the exp(i pi 64 m / N) part of the negacyclic twist, which
+// depends only on the register index m and is therefore a compile-time constant.
+TFB_HD cd fold_twist(int m) {
+  const double C[9] = {1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025452,
+                       0.7071067811865476, 0.5555702330196022, 0.3826834323650898, 0.19509032201612828,
+                       0.0};
+  return cd{C[m], C[8 - m]};  // (cos, sin)(pi m / 16)
+}
+
+// Spectral index held by (thread t, register k2) after a forward transform.
+TFB_HD int spectral_index(int t, int k2) { return (t >> 3) + 8 * (t & 7) + 64 * k2; }
+
+// Forward negacyclic transform, unnormalised.
+//   in : x[m] = c_{t+64m} = a_{t+64m} + i a_{t+64m+512}   (untwisted)
+//   out: x[k2] = Z[spectral_index(t, k2)],
+//        Z_k = sum_j c_j exp(i pi j / N) exp(2 pi i j k / 512)
+// bufA/bufB: 512 cd each in shared memory.
+template <class Sync>
+TFB_HD void fft_forward(cd* x, int t, const Twiddles* tw, cd* bufA, cd* bufB, Sync& sync) {
+#pragma unroll
+  for (int m = 1; m < 8; ++m) x[m] = cmul(x[m], fold_twist(m));
+  dft8<1>(x);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) bufA[64 * k + t] = cmul(x[k], tw->tw1[k][t]);
+  sync();
+  const int hi = t >> 3, lo = t & 7;
+#pragma unroll
+  for (int j1 = 0; j1 < 8; ++j1) x[j1] = bufA[64 * hi + 8 * j1 + lo];
+  dft8<1>(x);
+  bufB[64 * hi + lo] = x[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) bufB[64 * hi + 8 * k + (lo ^ k)] = cmul(x[k], tw->tw2[k][lo]);
+  sync();
+#pragma unroll
+  for (int j0 = 0; j0 < 8; ++j0) x[j0] = bufB[64 * hi + 8 * lo + (j0 ^ lo)];
+  dft8<1>(x);
+}
+
+// Inverse of fft_forward up to the factor 512 (folded into the key).
+//   in : x[k2] = S[spectral_index(t, k2)]
+//   out: x[m]  = c_{t+64m}  (re -> coefficient t+64m, im -> coefficient t+64m+512)
+template <class Sync>
+TFB_HD void fft_inverse(cd* x, int t, const Twiddles* tw, cd* bufA, cd* bufB, Sync& sync) {
+  const int hi = t >> 3, lo = t & 7;
+  dft8<-1>(x);
+  bufA[64 * hi + 8 * lo + lo] = x[0];
+#pragma unroll
+  for (int j0 = 1; j0 < 8; ++j0) bufA[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x[j0], tw->tw2[j0][lo]);
+  sync();
+#pragma unroll
+  for (int k1 = 0; k1 < 8; ++k1) x[k1] = bufA[64 * hi + 8 * k1 + (lo ^ k1)];
+  dft8<-1>(x);
+#pragma unroll
+  for (int j1 = 0; j1 < 8; ++j1) bufB[64 * hi + 8 * j1 + lo] = x[j1];
+  sync();
+#pragma unroll
+  for (int k0 = 0; k0 < 8; ++k0) x[k0] = cmulc(bufB[64 * k0 + t], tw->tw1[k0][t]);
+  dft8<-1>(x);
+#pragma unroll
+  for (int m = 1; m < 8; ++m) x[m] = cmulc(x[m], fold_twist(m));
+}
+
+// ---- rotation and gadget decomposition -----------------------------------------
+// coefficient j of X^abar * P - P for P in shared memory (N words), abar in [0, 2N)
+TFB_HD uint32_t rotated_diff(const uint32_t* poly, int j, int abar) {
+  const int src = (j - abar) & (2 * RING_N - 1);
+  const uint32_t v = poly[src & (RING_N - 1)];
+  const uint32_t neg = (uint32_t)(src >> 10) & 1u;  // 1 when the wrap flips the sign
+  return ((v ^ (0u - neg)) + neg) - poly[j];
+}
+
+TFB_HD uint32_t digit_field(uint32_t v_plus_offset, int lvl) {
+  return (v_plus_offset >> (32 - (lvl + 1) * BK_BGBIT)) & ((1u << BK_BGBIT) - 1);
+}
+
+// ---- one CMux step -----------------------------------------------------------------
+// acc: 2 polynomials of N words in shared memory ([0..N) = a, [N..2N) = b).
+// bk : spectral key of this LWE index, laid out [row][k2][c][t] (cd), prescaled by 1/512.
+// Every thread of the 64-thread group calls this; `sync` is the group barrier.
+template <class Sync, class LoadBk>
+TFB_HD void cmux_step(uint32_t* acc, int abar, const cd* bk, int t, const Twiddles* tw, cd* bufA,
+                      cd* bufB, Sync& sync, LoadBk load_bk) {
+  cd out0[8], out1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) out0[k] = out1[k] = cd{0.0, 0.0};
+
+#pragma unroll 1
+  for (int p = 0; p < 2; ++p) {
+    uint32_t v[16];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      v[m] = rotated_diff(acc + p * RING_N, t + 64 * m, abar) + DECOMP_OFFSET;
+      v[8 + m] = rotated_diff(acc + p * RING_N, t + 64 * m + HALF_N, abar) + DECOMP_OFFSET;
+    }
+#pragma unroll
+    for (int lvl = 0; lvl < BK_L; ++lvl) {
+      cd x[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        x[m] = cd{digit_to_double(digit_field(v[m], lvl)), digit_to_double(digit_field(v[8 + m], lvl))};
+      fft_forward(x, t, tw, bufA, bufB, sync);
+      const cd* row = bk + (size_t)(p * BK_L + lvl) * (8 * 2 * FFT_THREADS);
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) {
+        cmac(out0[k2], x[k2], load_bk(row + (k2 * 2 + 0) * FFT_THREADS + t));
+        cmac(out1[k2], x[k2], load_bk(row + (k2 * 2 + 1) * FFT_THREADS + t));
+      }
+    }
+  }
+  fft_inverse(out0, t, tw, bufA, bufB, sync);
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    acc[t + 64 * m] += round_to_word(out0[m].re);
+    acc[t + 64 * m + HALF_N] += round_to_word(out0[m].im);
+  }
+  fft_inverse(out1, t, tw, bufA, bufB, sync);
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    acc[RING_N + t + 64 * m] += round_to_word(out1[m].re);
+    acc[RING_N + t + 64 * m + HALF_N] += round_to_word(out1[m].im);
+  }
+  sync();
+}
+
+// ---- gate table -----------------------------------------------------------------------
+// kind ids follow the reference's TWO_INPUT_KINDS order (encirc/engine.py:77-88):
+// 0 AND 1 OR 2 NAND 3 NOR 4 XOR 5 XNOR 6 ANDNY 7 ORNY; 8 = identity (standalone bootstrap).
+constexpr int NUM_KINDS = 9;
+TFB_HD void gate_coeffs(int kind, int32_t& cx, int32_t& cy, int32_t& off) {
+  const int8_t CX[NUM_KINDS] = {1, 1, -1, -1, 2, -2, -1, -1, 1};
+  const int8_t CY[NUM_KINDS] = {1, 1, -1, -1, 2, -2, 1, 1, 0};
+  const int8_t OF[NUM_KINDS] = {-1, 1, 1, -1, 2, -2, -1, 1, 0};
+  cx = CX[kind];
+  cy = CY[kind];
+  off = OF[kind];
+}
+
+// round(a * 2N / 2^32) mod 2N
+TFB_HD int mod_switch(uint32_t a) { return (int)((a + (1u << 20)) >> 21) & (2 * RING_N - 1); }
+
+// Whole gate bootstrap (without key switch) for one ciphertext by one 64-thread group.
+//   x_row, y_row: pool rows (n mask words then the body)
+//   sm_acc: 2N words, sm_abar: n+1 uint16, bufA/bufB: 512 cd each
+//   ext: N+1 words out (extracted LWE sample under the ring key)
+template <class Sync, class LoadBk>
+TFB_HD void gate_bootstrap(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu,
+                           const cd* bkf, const Twiddles* tw, uint32_t* sm_acc, uint16_t* sm_abar,
+                           cd* bufA, cd* bufB, uint32_t* ext, int t, Sync& sync, LoadBk load_bk) {
+  int32_t cx, cy, off;
+  gate_coeffs(kind, cx, cy, off);
+  for (int w = t; w <= n; w += FFT_THREADS) {
+    uint32_t v = (uint32_t)cx * x_row[w] + (uint32_t)cy * y_row[w];
+    if (w == n) v += (uint32_t)off * mu;
+    sm_abar[w] = (uint16_t)mod_switch(v);
+  }
+  sync();
+  // ACC = (0, X^{2N - bbar} * testvector), testvector = mu * (1 + X + ... + X^{N-1})
+  const int bbar = sm_abar[n];
+  for (int j = t; j < RING_N; j += FFT_THREADS) {
+    sm_acc[j] = 0;
+    const int src = (j + bbar) & (2 * RING_N - 1);  // j - (2N - bbar) mod 2N
+    sm_acc[RING_N + j] = (src < RING_N) ? mu : (0u - mu);
+  }
+  sync();
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    const int abar = sm_abar[i];
+    if (abar == 0) continue;  // uniform across the group
+    cmux_step(sm_acc, abar, bkf + (size_t)i * (BK_ROWS * 8 * 2 * FFT_THREADS), t, tw, bufA, bufB, sync,
+              load_bk);
+  }
+  // sample extract at coefficient 0: a'_0 = a_0, a'_j = -a_{N-j}; b' = b_0
+  for (int j = t; j < RING_N; j += FFT_THREADS) ext[j] = (j == 0) ? sm_acc[0] : (0u - sm_acc[RING_N - j]);
+  if (t == 0) ext[RING_N] = sm_acc[RING_N];
+}
+
+// ---- key switch ---------------------------------------------------------------------------
+// signed base-4 digits d_j in {-2,-1,0,1} of a (top KS_T*KS_BASEBIT bits, rounded):
+//   a ~= sum_j d_j * 2^(32 - (j+1)*KS_BASEBIT)
+constexpr uint32_t KS_ROUND = 1u << (32 - KS_T * KS_BASEBIT - 1);
+TFB_HD uint32_t ks_bias() {
+  uint32_t b = KS_ROUND;
+  for (int j = 0; j < KS_T; ++j) b += (uint32_t)(1u << (KS_BASEBIT - 1)) << (32 - (j + 1) * KS_BASEBIT);
+  return b;
+}
+TFB_HD int32_t ks_digit(uint32_t a_biased, int j) {
+  return (int32_t)((a_biased >> (32 - (j + 1) * KS_BASEBIT)) & ((1u << KS_BASEBIT) - 1)) -
+         (1 << (KS_BASEBIT - 1));
+}
+
+}  // namespace tfb

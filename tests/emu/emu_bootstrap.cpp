@@ -1,0 +1,135 @@
+// Host emulation of kernel K1: runs the exact __host__ __device__ code of
+// paper_2005_01945_b200/csrc/tfhe_device.cuh with 64 std::threads per
+// ciphertext and a pthread barrier standing in for __syncthreads().  Test
+// infrastructure only: lets the CPU test-suite check the kernel's index math,
+// twiddles, swizzles and rounding against the integer oracle without a GPU.
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <thread>
+#include <vector>
+
+#include "../../paper_2005_01945_b200/csrc/tfhe_device.cuh"
+
+using namespace tfb;
+
+namespace {
+struct BarrierSync {
+  pthread_barrier_t* b;
+  void operator()() const { pthread_barrier_wait(b); }
+};
+struct PlainLoad {
+  cd operator()(const cd* p) const { return *p; }
+};
+
+void fill_twiddles(Twiddles* tw) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int k = 0; k < 8; ++k)
+    for (int t = 0; t < FFT_THREADS; ++t) {
+      const long double ang = pi * (long double)(t * (1 + 4 * k)) / (long double)RING_N;
+      tw->tw1[k][t] = cd{(double)cosl(ang), (double)sinl(ang)};
+    }
+  for (int k = 0; k < 8; ++k)
+    for (int a = 0; a < 8; ++a) {
+      const long double ang = 2.0L * pi * (long double)(a * k) / 64.0L;
+      tw->tw2[k][a] = cd{(double)cosl(ang), (double)sinl(ang)};
+    }
+}
+
+template <class F>
+void run_group(F body) {
+  pthread_barrier_t bar;
+  pthread_barrier_init(&bar, nullptr, FFT_THREADS);
+  std::vector<std::thread> th;
+  for (int t = 0; t < FFT_THREADS; ++t) th.emplace_back([&, t] { BarrierSync s{&bar}; body(t, s); });
+  for (auto& x : th) x.join();
+  pthread_barrier_destroy(&bar);
+}
+}  // namespace
+
+extern "C" {
+
+// spectral key in the kernel's layout [n][4][8][2][64], prescaled by 1/512
+void emu_bk_transform(const int32_t* bk_raw, int n, double* bkf_out) {
+  Twiddles tw;
+  fill_twiddles(&tw);
+  cd* bkf = reinterpret_cast<cd*>(bkf_out);
+  std::vector<cd> bufA(HALF_N), bufB(HALF_N);
+  for (int64_t poly = 0; poly < (int64_t)n * BK_ROWS * 2; ++poly) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(bk_raw) + poly * RING_N;
+    const int c = (int)(poly & 1);
+    const int64_t ir = poly >> 1;
+    run_group([&](int t, BarrierSync& s) {
+      cd x[8];
+      for (int m = 0; m < 8; ++m)
+        x[m] = cd{int32_to_double(src[t + 64 * m]), int32_to_double(src[t + 64 * m + HALF_N])};
+      fft_forward(x, t, &tw, bufA.data(), bufB.data(), s);
+      for (int k2 = 0; k2 < 8; ++k2)
+        bkf[((ir * 8 + k2) * 2 + c) * FFT_THREADS + t] = cd{x[k2].re / HALF_N, x[k2].im / HALF_N};
+    });
+  }
+}
+
+// forward transform of one int32 polynomial, natural frequency order, unnormalised
+void emu_fft_forward(const int32_t* poly, double* spec_out) {
+  Twiddles tw;
+  fill_twiddles(&tw);
+  std::vector<cd> bufA(HALF_N), bufB(HALF_N);
+  cd* out = reinterpret_cast<cd*>(spec_out);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(poly);
+  run_group([&](int t, BarrierSync& s) {
+    cd x[8];
+    for (int m = 0; m < 8; ++m)
+      x[m] = cd{int32_to_double(src[t + 64 * m]), int32_to_double(src[t + 64 * m + HALF_N])};
+    fft_forward(x, t, &tw, bufA.data(), bufB.data(), s);
+    for (int k2 = 0; k2 < 8; ++k2) out[spectral_index(t, k2)] = x[k2];
+  });
+}
+
+// inverse of emu_fft_forward (divides by 512), rounded to words
+void emu_fft_inverse(const double* spec_in, uint32_t* poly_out) {
+  Twiddles tw;
+  fill_twiddles(&tw);
+  std::vector<cd> bufA(HALF_N), bufB(HALF_N);
+  const cd* in = reinterpret_cast<const cd*>(spec_in);
+  run_group([&](int t, BarrierSync& s) {
+    cd x[8];
+    for (int k2 = 0; k2 < 8; ++k2) {
+      cd v = in[spectral_index(t, k2)];
+      x[k2] = cd{v.re / HALF_N, v.im / HALF_N};
+    }
+    fft_inverse(x, t, &tw, bufA.data(), bufB.data(), s);
+    for (int m = 0; m < 8; ++m) {
+      poly_out[t + 64 * m] = round_to_word(x[m].re);
+      poly_out[t + 64 * m + HALF_N] = round_to_word(x[m].im);
+    }
+  });
+}
+
+// K1 for k ciphertexts: x, y packed [k][n+1]; ext_out [k][N+1]
+void emu_gate_bootstrap(const uint32_t* x, const uint32_t* y, const uint8_t* kinds, int64_t k, int n,
+                        uint32_t mu, const double* bkf_in, uint32_t* ext_out) {
+  Twiddles tw;
+  fill_twiddles(&tw);
+  const cd* bkf = reinterpret_cast<const cd*>(bkf_in);
+  for (int64_t g = 0; g < k; ++g) {
+    std::vector<cd> bufA(HALF_N), bufB(HALF_N);
+    std::vector<uint32_t> acc(2 * RING_N), ext(EXT_STRIDE);
+    std::vector<uint16_t> abar(n + 1);
+    run_group([&](int t, BarrierSync& s) {
+      gate_bootstrap(x + g * (n + 1), y + g * (n + 1), (int)kinds[g], n, mu, bkf, &tw, acc.data(), abar.data(),
+                     bufA.data(), bufB.data(), ext.data(), t, s, PlainLoad());
+    });
+    for (int j = 0; j <= RING_N; ++j) ext_out[g * (RING_N + 1) + j] = ext[j];
+  }
+}
+
+// key-switch digits exactly as K2 derives them: digits_out[N][KS_T]
+void emu_ks_digits(const uint32_t* ext, int32_t* digits_out) {
+  const uint32_t bias = ks_bias();
+  for (int i = 0; i < RING_N; ++i)
+    for (int j = 0; j < KS_T; ++j) digits_out[i * KS_T + j] = ks_digit(ext[i] + bias, j);
+}
+}
