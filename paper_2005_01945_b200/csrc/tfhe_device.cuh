@@ -275,12 +275,14 @@ TFB_HD void cmux_step(uint32_t* acc, int abar, const cd* bk, int t, const Twiddl
 // 0 AND 1 OR 2 NAND 3 NOR 4 XOR 5 XNOR 6 ANDNY 7 ORNY; 8 = identity (standalone bootstrap).
 constexpr int NUM_KINDS = 9;
 TFB_HD void gate_coeffs(int kind, int32_t& cx, int32_t& cy, int32_t& off) {
-  const int8_t CX[NUM_KINDS] = {1, 1, -1, -1, 2, -2, -1, -1, 1};
-  const int8_t CY[NUM_KINDS] = {1, 1, -1, -1, 2, -2, 1, 1, 0};
-  const int8_t OF[NUM_KINDS] = {-1, 1, 1, -1, 2, -2, -1, 1, 0};
-  cx = CX[kind];
-  cy = CY[kind];
-  off = OF[kind];
+  // 4-bit biased nibbles (value + 8), kind 0 in the low nibble:
+  //   cx  = { 1, 1,-1,-1, 2,-2,-1,-1, 1}
+  //   cy  = { 1, 1,-1,-1, 2,-2, 1, 1, 0}
+  //   off = {-1, 1, 1,-1, 2,-2,-1, 1, 0}
+  const uint64_t CX = 0x9776A7799ull, CY = 0x8996A7799ull, OF = 0x8976A7997ull;
+  cx = (int32_t)((CX >> (4 * kind)) & 15) - 8;
+  cy = (int32_t)((CY >> (4 * kind)) & 15) - 8;
+  off = (int32_t)((OF >> (4 * kind)) & 15) - 8;
 }
 
 // round(a * 2N / 2^32) mod 2N
