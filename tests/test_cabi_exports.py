@@ -1,0 +1,64 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU and exports every
+symbol include/tfhe_b200.h declares (no compute calls here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2005_01945_b200 import _cabi
+
+
+@pytest.fixture(scope="module")
+def library():
+    _cabi.build_library()
+    return ctypes.CDLL(_cabi.LIB_PATH)
+
+
+def declared_symbols():
+    text = open(os.path.join(_cabi.INCLUDE, "tfhe_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(tfb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported(library):
+    names = declared_symbols()
+    assert len(names) >= 14
+    for name in names:
+        assert hasattr(library, name), name
+    assert set(names) == set(_cabi.EXPORTS)
+
+
+def test_abi_version_and_constants(library):
+    assert library.tfb_abi_version() == _cabi.ABI_VERSION
+    text = open(os.path.join(_cabi.INCLUDE, "tfhe_b200.h")).read()
+    assert f"#define TFB_ROW_STRIDE {_cabi.ROW_STRIDE}" in text
+    assert f"#define TFB_EXT_STRIDE {_cabi.EXT_STRIDE}" in text
+
+
+def test_binary_targets_sm_100a(library):
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "-lelf", _cabi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_unsupported_parameters_are_rejected_without_a_gpu(library):
+    bad = _cabi.tfb_params(500, 2048, 2, 10, 8, 2, 1 << 29)
+    handle = ctypes.c_void_p()
+    library.tfb_ctx_create.argtypes = [ctypes.c_int, ctypes.POINTER(_cabi.tfb_params), ctypes.POINTER(ctypes.c_void_p)]
+    assert library.tfb_ctx_create(0, ctypes.byref(bad), ctypes.byref(handle)) == 1  # TFB_ERR_INVALID
+    library.tfb_last_error.restype = ctypes.c_char_p
+    library.tfb_last_error.argtypes = [ctypes.c_void_p]
+    assert b"unsupported" in library.tfb_last_error(None)
+
+
+def test_engine_refuses_to_run_without_cuda(key):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2005_01945_b200 import B200Engine
+
+    with pytest.raises(_cabi.TfbError):
+        B200Engine(key, seed=1)

@@ -1,0 +1,177 @@
+"""B200Engine behind the reference's GateEngine API: the engine-contract checks
+of tests/test_engine_cpu.py re-run on the GPU engine, golden vectors of the
+reference, circuits against native arithmetic with the reference's counts."""
+import numpy as np
+import pytest
+
+from paper_2005_01945_b200 import (
+    BootstrapMarginError, EncBit, GateKind, LweSample, PoolConfig, WorkerPool, add_bitwise, decrypt_int,
+    decrypt_matrix, decrypt_vector, encrypt_int, encrypt_matrix, encrypt_vector, mat_mul_cannon,
+    mat_mul_flat, mul_karatsuba, mul_naive, vec_add, vec_mul,
+)
+from tests.test_circuits_cpu import check_scalar_circuits_against_reference
+from tests.test_engine_cpu import (
+    check_argument_errors, check_compound_economy, check_fresh_bound_and_bootstrap, check_not_is_free,
+    check_truth_tables,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def test_native_library_is_loaded(b200):
+    import ctypes
+
+    from paper_2005_01945_b200 import _cabi
+
+    assert isinstance(_cabi.lib(), ctypes.CDLL)
+    assert b200.kernel_launches >= 2  # key setup ran on the device
+
+
+def test_engine_contract(b200):
+    check_truth_tables(b200)
+    check_not_is_free(b200)
+    check_compound_economy(b200)
+    check_fresh_bound_and_bootstrap(b200)
+    check_argument_errors(b200)
+
+
+def test_fresh_ciphertexts_are_the_references(key, eval_keys, golden):
+    """Engine seed 5: the first encryptions are word-for-word the reference's
+    (encirc/engine.py:424,429-430)."""
+    from paper_2005_01945_b200 import B200Engine
+
+    eng = B200Engine(key, seed=5, eval_keys=eval_keys)
+    bits = [eng.encrypt(int(b)) for b in golden["enc5_bits"]]
+    for bit, want in zip(bits, golden["enc5_words"]):
+        s = bit.sample
+        assert np.array_equal(s.a, want[:-1]) and s.b == int(want[-1])
+        assert s.noise_bound == eng.fresh_bound and s.w == 32
+    assert [eng.decrypt(b) for b in bits] == golden["enc5_bits"].tolist()
+    # the reference's oracle launch on the same inputs decrypts to the same bits
+    eng = B200Engine(key, seed=5, eval_keys=eval_keys)
+    xs = [eng.encrypt((i >> 1) & 1) for i in range(32)]
+    ys = [eng.encrypt(i & 1) for i in range(32)]
+    from paper_2005_01945_b200.engine import TWO_INPUT_KINDS
+    from paper_2005_01945_b200 import JobBatch
+
+    outs = eng.pool.execute_batch(JobBatch([TWO_INPUT_KINDS[i // 4] for i in range(32)], xs, ys), eng)
+    assert [eng.decrypt(c) for c in outs] == golden["launch_out_bits"].tolist()
+    assert np.array_equal(np.stack([np.append(c.sample.a, c.sample.b) for c in xs]), golden["launch_x_words"])
+
+
+def test_margin_errors_and_adopted_samples(b200):
+    mu = b200.params.mu_float
+    good = b200.encrypt(1)
+    s = good.sample
+    bad = EncBit(b200, sample=LweSample(s.a, s.b, mu, 32))
+    with pytest.raises(BootstrapMarginError):
+        b200.eval_gate(GateKind.AND, bad, b200.encrypt(1))
+    with pytest.raises(BootstrapMarginError):
+        b200.bootstrap(bad)
+    ok = EncBit(b200, sample=LweSample(s.a, s.b, s.noise_bound, 32))
+    assert b200.decrypt(b200.eval_gate(GateKind.AND, ok, good)) == 1
+
+
+def test_same_seed_same_ciphertexts_and_worker_independence(key, eval_keys):
+    from paper_2005_01945_b200 import B200Engine
+
+    outs = []
+    for workers in (1, 8):
+        eng = B200Engine(key, seed=77, pool=WorkerPool(PoolConfig(workers=workers)), eval_keys=eval_keys)
+        xs = [eng.encrypt(i % 2) for i in range(300)]
+        ys = [eng.encrypt((i // 2) % 2) for i in range(300)]
+        got = eng.eval_gate_batch(GateKind.NAND, xs, ys)
+        assert eng.snapshot_stats().batch_launches == 1
+        outs.append(eng.read_rows([b.row for b in got]).tobytes())
+        assert [eng.decrypt(b) for b in got] == [1 - ((i % 2) & ((i // 2) % 2)) for i in range(300)]
+    assert outs[0] == outs[1]
+
+
+def test_scalar_circuits_counts_and_results(b200, golden):
+    check_scalar_circuits_against_reference(b200, golden, widths=(8, 16))
+
+
+def test_random_circuits_agree_with_cleartext_engine(b200):
+    from paper_2005_01945_b200 import ReferenceEngine
+    from paper_2005_01945_b200.engine import TWO_INPUT_KINDS
+
+    rng = np.random.default_rng(5)
+    for trial in range(6):
+        ref = ReferenceEngine(b200.params)
+        engines = (ref, b200)
+        for e in engines:
+            e.reset_stats()
+        inputs = rng.integers(0, 2, size=6).tolist()
+        wires = [[e.encrypt(v) for v in inputs] for e in engines]
+        for _ in range(20):
+            op = rng.integers(0, 3)
+            i, j = rng.integers(0, len(wires[0]), size=2)
+            ka, kb = (TWO_INPUT_KINDS[t] for t in rng.integers(0, 8, size=2))
+            for e, w in zip(engines, wires):
+                if op == 0:
+                    w.append(e.eval_gate(ka, w[i], w[j]))
+                elif op == 1:
+                    w.extend(e.eval_compound(ka, kb, w[i], w[j]))
+                else:
+                    w.append(e.eval_not(w[i]))
+        assert [ref.decrypt(b) for b in wires[0]] == [b200.decrypt(b) for b in wires[1]]
+        assert ref.stats.as_record() == b200.stats.as_record()
+
+
+def test_arithmetic_16_and_32_bit(b200):
+    rng = np.random.default_rng((11, 2))
+    for n in (16, 32):
+        a, b = int(rng.integers(0, 1 << n, dtype=np.uint64)), int(rng.integers(0, 1 << n, dtype=np.uint64))
+        x, y = encrypt_int(b200, a, n), encrypt_int(b200, b, n)
+        b200.reset_stats()
+        assert decrypt_int(b200, add_bitwise(x, y)) == (a + b) % (1 << n)
+        assert (b200.stats.bootstraps, b200.stats.batch_launches) == (5 * n, 3 * n)
+        b200.reset_stats()
+        assert decrypt_int(b200, mul_naive(x, y)) == a * b
+        assert b200.stats.bootstraps == 11 * n * n - 10 * n
+    a, b = 40503, 65535
+    x, y = encrypt_int(b200, a, 16), encrypt_int(b200, b, 16)
+    assert decrypt_int(b200, mul_karatsuba(x, y)) == a * b
+
+
+def test_vectors_and_matrices(b200):
+    rng = np.random.default_rng(21)
+    u = rng.integers(0, 1 << 16, size=24).tolist()
+    v = rng.integers(0, 1 << 16, size=24).tolist()
+    eu, ev = encrypt_vector(b200, u, 16), encrypt_vector(b200, v, 16)
+    b200.reset_stats()
+    assert decrypt_vector(b200, vec_add(eu, ev)) == [(a + b) % (1 << 16) for a, b in zip(u, v)]
+    assert b200.stats.batch_launches == 48
+    assert decrypt_vector(b200, vec_mul(eu, ev)) == [a * b for a, b in zip(u, v)]
+    A = rng.integers(0, 1 << 16, size=(3, 3)).tolist()
+    B = rng.integers(0, 1 << 16, size=(3, 3)).tolist()
+    want = [[sum(A[i][t] * B[t][j] for t in range(3)) % (1 << 16) for j in range(3)] for i in range(3)]
+    ea, eb = encrypt_matrix(b200, A, 16), encrypt_matrix(b200, B, 16)
+    assert decrypt_matrix(b200, mat_mul_flat(ea, eb)) == want
+    assert decrypt_matrix(b200, mat_mul_cannon(ea, eb)) == want
+
+
+def test_noise_hygiene_over_many_gate_outputs(b200):
+    """10,000 chained gate outputs: all decrypt correctly and every phase stays
+    within the declared fresh bound of +-mu (reference acceptance :328-374)."""
+    rng = np.random.default_rng(9)
+    bits = rng.integers(0, 2, size=2500)
+    rows, own = b200.encrypt_rows(bits.tolist())
+    clear = bits.copy()
+    seen = 0
+    for step in range(4):
+        perm = rng.permutation(len(rows))
+        kind = (GateKind.NAND, GateKind.XOR, GateKind.ORNY, GateKind.XNOR)[step]
+        out, own2 = b200.gate_rows(kind, rows, rows[perm])
+        from paper_2005_01945_b200 import truth_table
+
+        tt = np.array(truth_table(kind))
+        clear = tt[(clear << 1) | clear[perm]]
+        ph = b200.phases(out).astype(np.int64)
+        target = np.where(clear == 1, 1 << 29, (1 << 32) - (1 << 29))
+        err = ((ph - target + 2**31) % 2**32) - 2**31
+        assert np.abs(err).max() < (1 << 27)
+        assert np.array_equal(b200.decrypt_rows(out), clear)
+        rows, own = out, own2
+        seen += len(out)
+    assert seen == 10000

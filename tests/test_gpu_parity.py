@@ -1,0 +1,173 @@
+"""CUDA path against the CPU oracle through the C ABI, stage by stage, bit-exact.
+
+Integer / torus-word work: the bar is bit-exact.  The FP64 FFT inside kernel K1
+is an implementation detail whose rounded output must equal the exact integer
+product; the spectral key is compared with numpy within 1e-13 relative."""
+import numpy as np
+import pytest
+
+from oracle import tfhe_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def pack(s):
+    return np.concatenate([s.a, [s.b]]).astype(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def gpu(key, eval_keys):
+    import torch
+
+    from paper_2005_01945_b200 import _cabi
+
+    ctx = _cabi.Context(0, key.params.m, key.params.mu.word, eval_keys.ring)
+    ctx.call("tfb_load_keys", eval_keys.bk.ctypes.data, eval_keys.ksk.ctypes.data, 0, None)
+    return ctx, torch, _cabi
+
+
+def make_inputs(key, K, seed, kinds=None):
+    from paper_2005_01945_b200 import encrypt_bit
+
+    rng = np.random.default_rng((seed, 0))
+    bits = np.random.default_rng((seed, 2)).integers(0, 2, size=(2, K))
+    xs = np.stack([pack(encrypt_bit(key, int(b), rng)) for b in bits[0]])
+    ys = np.stack([pack(encrypt_bit(key, int(b), rng)) for b in bits[1]])
+    if kinds is None:
+        kinds = (np.arange(K) % 8).astype(np.uint8)
+    return xs, ys, kinds, bits
+
+
+def run_launch(gpu, key, xs, ys, kinds, taps=False):
+    ctx, torch, _cabi = gpu
+    K, n = len(xs), key.params.m
+    dev = torch.device("cuda:0")
+    pool = torch.zeros((3 * K, _cabi.ROW_STRIDE), dtype=torch.int32, device=dev)
+    pool[:K, : n + 1] = torch.from_numpy(xs.view(np.int32)).to(dev)
+    pool[K : 2 * K, : n + 1] = torch.from_numpy(ys.view(np.int32)).to(dev)
+    kd = torch.from_numpy(kinds).to(dev)
+    idx = torch.arange(0, 3 * K, dtype=torch.int32, device=dev)
+    xr, yr, orow = idx[:K], idx[K : 2 * K], idx[2 * K :]
+    if taps:
+        ext = torch.zeros((K, _cabi.EXT_STRIDE), dtype=torch.int32, device=dev)
+        ctx.call("tfb_debug_blind_rotate", pool.data_ptr(), kd.data_ptr(), xr.data_ptr(), yr.data_ptr(), ext.data_ptr(), K, None)
+        ctx.call("tfb_debug_key_switch", ext.data_ptr(), pool.data_ptr(), orow.data_ptr(), K, None)
+        torch.cuda.synchronize()
+        return pool[2 * K :, : n + 1].cpu().numpy().view(np.uint32), ext.cpu().numpy().view(np.uint32)[:, :1025]
+    ctx.call("tfb_gate_launch", pool.data_ptr(), kd.data_ptr(), xr.data_ptr(), yr.data_ptr(), orow.data_ptr(), K, None)
+    torch.cuda.synchronize()
+    return pool[2 * K :, : n + 1].cpu().numpy().view(np.uint32)
+
+
+def test_spectral_key_matches_numpy(gpu, eval_keys):
+    ctx, torch, _cabi = gpu
+    N = 1024
+    tw = np.exp(1j * np.pi * np.arange(N // 2) / N)
+    for i in (0, 3, 499):
+        spec = np.empty((4, 2, 512, 2), dtype=np.float64)
+        ctx.call("tfb_debug_spectral_key", i, spec.ctypes.data)
+        poly = eval_keys.bk[i].astype(np.float64)
+        want = np.fft.ifft((poly[..., : N // 2] + 1j * poly[..., N // 2 :]) * tw, axis=-1) * (N // 2)
+        got = spec[..., 0] + 1j * spec[..., 1]
+        assert np.abs(got - want).max() / np.abs(want).max() < 1e-13
+
+
+def test_blind_rotate_and_key_switch_bit_exact(gpu, key, eval_keys):
+    xs, ys, kinds, bits = make_inputs(key, 24, seed=31)
+    want_out, want_ext = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk,
+                                                  fft=True, want_ext=True)
+    got_out, got_ext = run_launch(gpu, key, xs, ys, kinds, taps=True)
+    assert np.array_equal(got_ext, want_ext)
+    assert np.array_equal(got_out, want_out)
+    # cross-check a few of the oracle's fft-path results with its exact integer path
+    exact = orc.gate_bootstrap_batch(xs[:3], ys[:3], kinds[:3], key.params.mu.word, eval_keys.bk, eval_keys.ksk)
+    assert np.array_equal(exact, want_out[:3])
+
+
+def test_fused_launch_all_kinds_and_identity(gpu, key, eval_keys):
+    K = 72
+    kinds = (np.arange(K) % 9).astype(np.uint8)  # includes kind 8 = identity refresh
+    xs, ys, kinds, bits = make_inputs(key, K, seed=32, kinds=kinds)
+    want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
+    got = run_launch(gpu, key, xs, ys, kinds)
+    assert np.array_equal(got, want)
+
+
+def test_host_buffer_entry_point(gpu, key, eval_keys):
+    ctx, torch, _cabi = gpu
+    xs, ys, kinds, bits = make_inputs(key, 40, seed=33)
+    want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
+    out = np.zeros_like(xs)
+    ctx.call("tfb_gate_launch_host", xs.ctypes.data, ys.ctypes.data, kinds.ctypes.data, out.ctypes.data, len(xs))
+    assert np.array_equal(out, want)
+    # ragged second call reuses the buffers
+    out2 = np.zeros_like(xs[:7])
+    ctx.call("tfb_gate_launch_host", xs[:7].ctypes.data, ys[:7].ctypes.data, kinds[:7].ctypes.data, out2.ctypes.data, 7)
+    assert np.array_equal(out2, want[:7])
+
+
+def test_edge_inputs_trivial_and_aliased(gpu, key, eval_keys):
+    p = key.params
+    t1 = np.zeros(501, dtype=np.uint32); t1[-1] = p.message_word(1)
+    t0 = np.zeros(501, dtype=np.uint32); t0[-1] = p.message_word(0)
+    xs0, ys0, _, _ = make_inputs(key, 4, seed=34)
+    xs = np.stack([t1, t0, xs0[0], t1, xs0[1], xs0[2]])
+    ys = np.stack([t0, t0, t1, xs0[3], xs0[1], ys0[2]])  # job 4 feeds the same sample twice
+    kinds = np.array([0, 1, 4, 6, 4, 5], dtype=np.uint8)
+    want = orc.gate_bootstrap_batch(xs, ys, kinds, p.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
+    got = run_launch(gpu, key, xs, ys, kinds)
+    assert np.array_equal(got, want)
+    assert not got[0, :-1].any() and int(got[0, -1]) == p.message_word(0)  # AND(1, 0) of trivials stays trivial
+
+
+def test_invalid_calls_return_status(gpu):
+    ctx, torch, _cabi = gpu
+    with pytest.raises(_cabi.TfbError):
+        ctx.call("tfb_gate_launch", None, None, None, None, None, 4, None)
+    with pytest.raises(_cabi.TfbError):
+        ctx.call("tfb_gate_launch_host", None, None, None, None, 0)
+
+
+def test_full_size_launch_properties(gpu, key, eval_keys):
+    """2**16 gates in one launch (BASELINE configs[1]): every output decrypts to
+    its truth table, every phase sits within the reference's fresh bound of
+    +-mu, and a sample of rows equals the oracle bit for bit."""
+    ctx, torch, _cabi = gpu
+    K, n = 1 << 16, key.params.m
+    base = 256
+    xs, ys, kinds, bits = make_inputs(key, base, seed=35)
+    dev = torch.device("cuda:0")
+    rep = torch.arange(K, device=dev) % base
+    pool = torch.zeros((3 * K, _cabi.ROW_STRIDE), dtype=torch.int32, device=dev)
+    pool[:K, : n + 1] = torch.from_numpy(xs.view(np.int32)).to(dev)[rep]
+    # pair x_g with y_{(g // base + g) % base} so the 2**16 jobs are distinct combinations
+    yidx = (torch.arange(K, device=dev) // base + torch.arange(K, device=dev)) % base
+    pool[K : 2 * K, : n + 1] = torch.from_numpy(ys.view(np.int32)).to(dev)[yidx]
+    kd = (torch.arange(K, device=dev) % 8).to(torch.uint8)
+    idx = torch.arange(0, 3 * K, dtype=torch.int32, device=dev)
+    ctx.call("tfb_gate_launch", pool.data_ptr(), kd.data_ptr(), idx[:K].data_ptr(), idx[K : 2 * K].data_ptr(),
+             idx[2 * K :].data_ptr(), K, None)
+    kb = torch.from_numpy(key.bits.astype(np.uint32).view(np.int32)).to(dev)
+    ph = torch.empty(K, dtype=torch.int32, device=dev)
+    ctx.call("tfb_rows_phase", pool.data_ptr(), idx[2 * K :].data_ptr(), kb.data_ptr(), ph.data_ptr(), K, None)
+    torch.cuda.synchronize()
+    phase = ph.cpu().numpy().view(np.uint32).astype(np.int64)
+    from paper_2005_01945_b200.engine import TWO_INPUT_KINDS, truth_table
+
+    g = np.arange(K)
+    bx, by = bits[0][g % base], bits[1][(g // base + g) % base]
+    tt = np.array([truth_table(k) for k in TWO_INPUT_KINDS])
+    want_bit = tt[g % 8, (bx << 1) | by]
+    got_bit = ((phase > 0) & (phase < 2**31)).astype(np.int64)
+    assert np.array_equal(got_bit, want_bit)
+    target = np.where(want_bit == 1, 1 << 29, (1 << 32) - (1 << 29))
+    err = ((phase - target + 2**31) % 2**32) - 2**31
+    assert np.abs(err).max() < (1 << 27)  # fresh_noise_bound = 2**-5 (encirc/torus.py:177-184)
+    # bit-exact sample against the oracle
+    sel = np.array([0, 1, 255, 256, 4097, 65535])
+    sx = xs[sel % base]
+    sy = ys[(sel // base + sel) % base]
+    want = orc.gate_bootstrap_batch(sx, sy, (sel % 8).astype(np.uint8), key.params.mu.word, eval_keys.bk,
+                                    eval_keys.ksk, fft=True)
+    got = pool[2 * K + torch.from_numpy(sel).to(dev), : n + 1].cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, want)
