@@ -13,7 +13,7 @@ import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(_HERE, "csrc")
-LIB_PATH = os.path.join(CSRC, "libtfhe_b200.so")
+LIB_PATH = os.environ.get("TFB_LIB") or os.path.join(CSRC, "libtfhe_b200.so")  # TFB_LIB: A/B builds
 INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 
 ROW_STRIDE = 512

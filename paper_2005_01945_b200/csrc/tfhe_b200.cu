@@ -45,6 +45,8 @@ struct tfb_ctx {
   int32_t* d_hrows = nullptr;  // identity row indices
   int64_t host_cap = 0;
   int64_t launches = 0;
+  int sm_count = 148;
+  int force_kernel = 0;        // 0 auto, 1 = K1a (one ciphertext per CTA), 2 = K1b (ring)
   std::string err;
 };
 
@@ -62,33 +64,186 @@ static thread_local std::string g_create_err;
 struct BlockSync {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
-struct LdgBk {
-  __device__ __forceinline__ cd operator()(const cd* p) const {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
-    return cd{v.x, v.y};
+// named barrier over one 64-thread ciphertext group of a multi-group CTA
+struct GroupSync {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(FFT_THREADS) : "memory");
   }
 };
+// spectral key read straight from global memory through L1 (small launches)
+struct LdgBk {
+  const cd* base;
+  __device__ __forceinline__ const cd* acquire(int i, int p) { return base + stage_offset(i, p); }
+  __device__ __forceinline__ cd load(const cd* q) const {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(q));
+    return cd{v.x, v.y};
+  }
+  __device__ __forceinline__ void release() {}
+  __device__ __forceinline__ void skip(int) {}
+};
+
+// ---- mbarrier / bulk-copy (TMA) primitives --------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_LOOP:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra WAIT_LOOP;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (SASS: UBLKCP)
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 // ------------------------------------------------------------------------------------
-// K1: fused gate bootstrap (one ciphertext per 64-thread CTA)
+// K1a: fused gate bootstrap, one ciphertext per 64-thread CTA, key through L1/L2.
+//      Used for launches too small to fill the chip with K1b's 6-ciphertext CTAs.
 // ------------------------------------------------------------------------------------
-constexpr int K1_SMEM_FIXED = 2 * HALF_N * (int)sizeof(cd) + 2 * RING_N * (int)sizeof(uint32_t);
+// per-ciphertext smem: s0 | s1 | acc (2N words) | abar (n+1 uint16, padded)
+constexpr int GROUP_SMEM_FIXED = 2 * HALF_N * (int)sizeof(cd) + 2 * RING_N * (int)sizeof(uint32_t);
+__host__ __device__ constexpr int group_smem(int n) { return GROUP_SMEM_FIXED + ((n + 1) * 2 + 15) / 16 * 16; }
+#ifndef TFB_K1_MIN_BLOCKS
+#define TFB_K1_MIN_BLOCKS 6
+#endif
 
-__global__ void __launch_bounds__(FFT_THREADS) k_gate_bootstrap(
+__global__ void __launch_bounds__(FFT_THREADS, TFB_K1_MIN_BLOCKS) k_gate_bootstrap(
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
     const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
-    const cd* __restrict__ bkf, const Twiddles* __restrict__ tw, uint32_t* __restrict__ ext) {
+    const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext) {
   extern __shared__ __align__(16) unsigned char smem[];
-  cd* bufA = reinterpret_cast<cd*>(smem);
-  cd* bufB = bufA + HALF_N;
-  uint32_t* acc = reinterpret_cast<uint32_t*>(bufB + HALF_N);
+  Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
+  cd* s0 = reinterpret_cast<cd*>(smem + sizeof(Twiddles));
+  cd* s1 = s0 + HALF_N;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(s1 + HALF_N);
   uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
+  for (int i = threadIdx.x; i < (int)(sizeof(Twiddles) / sizeof(cd)); i += FFT_THREADS)
+    reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
   const int64_t g = blockIdx.x;
   const uint32_t* xr = pool + (int64_t)x_rows[g] * ROW_STRIDE;
   const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
   BlockSync sync;
-  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bkf, tw, acc, abar, bufA, bufB, ext + g * EXT_STRIDE,
-                 (int)threadIdx.x, sync, LdgBk());
+  LdgBk bk{bkf};
+  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, ext + g * EXT_STRIDE,
+                 (int)threadIdx.x, sync);
+}
+
+// ------------------------------------------------------------------------------------
+// K1b: fused gate bootstrap, K1B_GROUPS ciphertexts per CTA (one CTA per SM).
+//      The spectral key is staged through a two-slot shared-memory ring by bulk
+//      copies (TMA), one 32 KB stage per (LWE index, accumulator polynomial), and
+//      shared by all groups of the CTA: L2->SM key traffic drops by the group count
+//      and the key is resident before any group needs it.  Groups synchronise only
+//      through the ring's full/empty mbarriers, so they drift apart by up to one
+//      stage and their FP64-heavy and LSU-heavy phases overlap.
+// ------------------------------------------------------------------------------------
+#ifndef TFB_K1B_GROUPS
+#define TFB_K1B_GROUPS 6
+#endif
+constexpr int K1B_GROUPS = TFB_K1B_GROUPS;
+constexpr int K1B_THREADS = K1B_GROUPS * FFT_THREADS;
+constexpr int STAGE_BYTES = STAGE_CD * (int)sizeof(cd);
+// dynamic smem: twiddles | ring[2][STAGE_CD] | mbarriers (64 B) | groups
+constexpr int K1B_HEADER = (int)sizeof(Twiddles) + 2 * STAGE_BYTES + 64;
+
+struct RingBk {
+  const cd* bkf;       // full spectral key in global memory
+  cd* ring;            // 2 stages in shared memory
+  uint64_t* full;      // [2] completes when a stage's bytes have landed
+  uint64_t* empty;     // [2] completes when every warp of the CTA released the stage
+  int stage;           // next stage this thread will consume (2*i + p)
+  int n_stages;
+  bool producer;       // exactly one thread of the CTA issues the copies
+
+  __device__ __forceinline__ void issue(int s) {
+    mbar_expect_tx(&full[s & 1], STAGE_BYTES);
+    bulk_load(ring + (size_t)(s & 1) * STAGE_CD, bkf + (size_t)s * STAGE_CD, STAGE_BYTES, &full[s & 1]);
+  }
+  // refill the slot stage-1 used with stage+1, once every warp has released it
+  __device__ __forceinline__ void produce_ahead() {
+    if (producer && stage >= 1 && stage + 1 < n_stages) {
+      const int prev = stage - 1;
+      mbar_wait(&empty[prev & 1], (uint32_t)(prev >> 1) & 1u);
+      issue(stage + 1);
+    }
+  }
+  __device__ __forceinline__ const cd* acquire(int, int) {
+    produce_ahead();
+    mbar_wait(&full[stage & 1], (uint32_t)(stage >> 1) & 1u);
+    return ring + (size_t)(stage & 1) * STAGE_CD;
+  }
+  __device__ __forceinline__ cd load(const cd* q) const { return *q; }
+  __device__ __forceinline__ void release() {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[stage & 1]);
+    ++stage;
+  }
+  __device__ __forceinline__ void skip(int) {
+    acquire(0, 0);
+    release();
+    acquire(0, 1);
+    release();
+  }
+};
+
+__global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
+    const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
+    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
+    const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext,
+    int64_t k) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
+  cd* ring = reinterpret_cast<cd*>(smem + sizeof(Twiddles));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sizeof(Twiddles) + 2 * STAGE_BYTES);
+  const int grp = threadIdx.x / FFT_THREADS, t = threadIdx.x % FFT_THREADS;
+  unsigned char* mine = smem + K1B_HEADER + (size_t)grp * group_smem(n);
+  cd* s0 = reinterpret_cast<cd*>(mine);
+  cd* s1 = s0 + HALF_N;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(s1 + HALF_N);
+  uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
+
+  for (int i = threadIdx.x; i < (int)(sizeof(Twiddles) / sizeof(cd)); i += K1B_THREADS)
+    reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
+  RingBk bk{bkf, ring, bars, bars + 2, 0, 2 * n, threadIdx.x == 0};
+  if (threadIdx.x == 0) {
+    mbar_init(&bk.full[0], 1);
+    mbar_init(&bk.full[1], 1);
+    mbar_init(&bk.empty[0], K1B_THREADS / 32);
+    mbar_init(&bk.empty[1], K1B_THREADS / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bk.issue(0);
+    bk.issue(1);
+  }
+  // tail CTA: surplus groups redo the last ciphertext (keeps the ring protocol uniform) but do not store
+  const int64_t want = (int64_t)blockIdx.x * K1B_GROUPS + grp;
+  const int64_t g = want < k ? want : k - 1;
+  const uint32_t* xr = pool + (int64_t)x_rows[g] * ROW_STRIDE;
+  const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
+  uint32_t* dst = want < k ? ext + g * EXT_STRIDE : reinterpret_cast<uint32_t*>(s0);  // scratch sink
+  GroupSync sync{grp + 1};
+  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, dst, t, sync);
 }
 
 // ------------------------------------------------------------------------------------
@@ -159,7 +314,7 @@ __global__ void __launch_bounds__(KS_THREADS) k_key_switch(const uint32_t* __res
 // ------------------------------------------------------------------------------------
 // K3: key setup
 // ------------------------------------------------------------------------------------
-// one CTA per raw polynomial: bk_raw[(i*4 + r)*2 + c][N] -> bkf[i][r][k2][c][t]
+// one CTA per raw polynomial: bk_raw[(i*4 + r)*2 + c][N] -> staged layout bkf[i][p][k2][lvl][c][t], r = p*l + lvl
 __global__ void __launch_bounds__(FFT_THREADS) k_bk_transform(const int32_t* __restrict__ bk_raw,
                                                               cd* __restrict__ bkf,
                                                               const Twiddles* __restrict__ tw) {
@@ -179,7 +334,8 @@ __global__ void __launch_bounds__(FFT_THREADS) k_bk_transform(const int32_t* __r
   const double scale = 1.0 / HALF_N;
 #pragma unroll
   for (int k2 = 0; k2 < 8; ++k2)
-    bkf[((ir * 8 + k2) * 2 + c) * FFT_THREADS + t] = cd{x[k2].re * scale, x[k2].im * scale};
+    bkf[stage_offset((int)(ir / BK_ROWS), (int)(ir % BK_ROWS) / BK_L) + stage_index(k2, (int)(ir % BK_L), c, t)] =
+        cd{x[k2].re * scale, x[k2].im * scale};
 }
 
 // ksk_raw[N*t][n+1] -> ksk[N*t][ROW_STRIDE], zero padded
@@ -304,12 +460,22 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
   if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw, h, sizeof(Twiddles), cudaMemcpyHostToDevice);
   delete h;
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_gate_bootstrap, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    e = cudaFuncSetAttribute(k_gate_bootstrap, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Twiddles) + group_smem(p->n));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gate_bootstrap_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             K1B_HEADER + K1B_GROUPS * group_smem(p->n));
+  if (e == cudaSuccess) {
+    int sms = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->sm_count = sms;
+  }
   if (e != cudaSuccess) {
     g_create_err = std::string("context setup: ") + cudaGetErrorString(e);
     delete ctx;
     return TFB_ERR_CUDA;
   }
+  if (const char* f = getenv("TFB_FORCE_KERNEL")) ctx->force_kernel = atoi(f);  // A/B switch for profiling
   *out = ctx;
   return TFB_OK;
 }
@@ -360,9 +526,18 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
 
 static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds, const int32_t* xr,
                                const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
-  const int smem = K1_SMEM_FIXED + ((ctx->p.n + 1) * 2 + 15) / 16 * 16;
-  k_gate_bootstrap<<<(unsigned)k, FFT_THREADS, smem, st>>>((const uint32_t*)pool, kinds, xr, yr, ctx->p.n,
-                                                           ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
+  const int n = ctx->p.n;
+  // K1b keeps K1B_GROUPS ciphertexts on one SM; below one full wave of such CTAs the
+  // one-ciphertext-per-CTA kernel spreads the launch over more SMs and wins.
+  const bool ring = ctx->force_kernel ? ctx->force_kernel == 2 : k >= (int64_t)ctx->sm_count * K1B_GROUPS;
+  if (ring) {
+    const unsigned grid = (unsigned)((k + K1B_GROUPS - 1) / K1B_GROUPS);
+    k_gate_bootstrap_ring<<<grid, K1B_THREADS, K1B_HEADER + K1B_GROUPS * group_smem(n), st>>>(
+        (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext, k);
+  } else {
+    k_gate_bootstrap<<<(unsigned)k, FFT_THREADS, (int)sizeof(Twiddles) + group_smem(n), st>>>(
+        (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
+  }
   ctx->launches += 1;
   TFB_CUDA(ctx, cudaGetLastError());
   return TFB_OK;
@@ -489,14 +664,14 @@ int tfb_debug_spectral_key(tfb_ctx* ctx, int32_t i, double* out) {
   if (!ctx || !out || i < 0 || i >= ctx->p.n) return TFB_ERR_INVALID;
   if (!ctx->keys_loaded) return TFB_ERR_STATE;
   TFB_CUDA(ctx, cudaSetDevice(ctx->device));
-  const size_t per_i = (size_t)BK_ROWS * 8 * 2 * FFT_THREADS;
+  const size_t per_i = (size_t)2 * STAGE_CD;
   std::vector<cd> h(per_i);
   TFB_CUDA(ctx, cudaMemcpy(h.data(), ctx->d_bkf + (size_t)i * per_i, per_i * sizeof(cd), cudaMemcpyDeviceToHost));
   for (int r = 0; r < BK_ROWS; ++r)
     for (int k2 = 0; k2 < 8; ++k2)
       for (int c = 0; c < 2; ++c)
         for (int t = 0; t < FFT_THREADS; ++t) {
-          const cd v = h[((size_t)(r * 8 + k2) * 2 + c) * FFT_THREADS + t];
+          const cd v = h[(size_t)(r / BK_L) * STAGE_CD + stage_index(k2, r % BK_L, c, t)];
           const int f = spectral_index(t, k2);
           double* dst = out + (((size_t)(r * 2 + c) * HALF_N) + f) * 2;
           dst[0] = v.re * HALF_N;

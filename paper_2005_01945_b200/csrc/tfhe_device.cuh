@@ -208,6 +208,100 @@ TFB_HD void fft_inverse(cd* x, int t, const Twiddles* tw, cd* bufA, cd* bufB, Sy
   for (int m = 1; m < 8; ++m) x[m] = cmulc(x[m], fold_twist(m));
 }
 
+// ---- paired transforms --------------------------------------------------------
+// Two independent transforms advanced in lock step by the same 64 threads: every
+// twiddle is loaded once and used twice, the barrier count per transform halves
+// and each thread carries twice the independent FP64 work between barriers.
+// s0/s1 are the exchange buffers of the two transforms (512 cd each); both
+// exchanges of a transform reuse its buffer, hence the barrier after each read.
+template <class Sync>
+TFB_HD void fft_forward2(cd* x0, cd* x1, int t, const Twiddles* tw, cd* s0, cd* s1, Sync& sync) {
+#pragma unroll
+  for (int m = 1; m < 8; ++m) {
+    x0[m] = cmul(x0[m], fold_twist(m));
+    x1[m] = cmul(x1[m], fold_twist(m));
+  }
+  dft8<1>(x0);
+  dft8<1>(x1);
+  sync();  // previous readers of s0/s1 are done
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const cd w = tw->tw1[k][t];
+    s0[64 * k + t] = cmul(x0[k], w);
+    s1[64 * k + t] = cmul(x1[k], w);
+  }
+  sync();
+  const int hi = t >> 3, lo = t & 7;
+#pragma unroll
+  for (int j1 = 0; j1 < 8; ++j1) {
+    x0[j1] = s0[64 * hi + 8 * j1 + lo];
+    x1[j1] = s1[64 * hi + 8 * j1 + lo];
+  }
+  dft8<1>(x0);
+  dft8<1>(x1);
+  sync();
+  s0[64 * hi + lo] = x0[0];
+  s1[64 * hi + lo] = x1[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) {
+    const cd w = tw->tw2[k][lo];
+    s0[64 * hi + 8 * k + (lo ^ k)] = cmul(x0[k], w);
+    s1[64 * hi + 8 * k + (lo ^ k)] = cmul(x1[k], w);
+  }
+  sync();
+#pragma unroll
+  for (int j0 = 0; j0 < 8; ++j0) {
+    x0[j0] = s0[64 * hi + 8 * lo + (j0 ^ lo)];
+    x1[j0] = s1[64 * hi + 8 * lo + (j0 ^ lo)];
+  }
+  dft8<1>(x0);
+  dft8<1>(x1);
+}
+
+template <class Sync>
+TFB_HD void fft_inverse2(cd* x0, cd* x1, int t, const Twiddles* tw, cd* s0, cd* s1, Sync& sync) {
+  const int hi = t >> 3, lo = t & 7;
+  dft8<-1>(x0);
+  dft8<-1>(x1);
+  sync();
+  s0[64 * hi + 8 * lo + lo] = x0[0];
+  s1[64 * hi + 8 * lo + lo] = x1[0];
+#pragma unroll
+  for (int j0 = 1; j0 < 8; ++j0) {
+    const cd w = tw->tw2[j0][lo];
+    s0[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x0[j0], w);
+    s1[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x1[j0], w);
+  }
+  sync();
+#pragma unroll
+  for (int k1 = 0; k1 < 8; ++k1) {
+    x0[k1] = s0[64 * hi + 8 * k1 + (lo ^ k1)];
+    x1[k1] = s1[64 * hi + 8 * k1 + (lo ^ k1)];
+  }
+  dft8<-1>(x0);
+  dft8<-1>(x1);
+  sync();
+#pragma unroll
+  for (int j1 = 0; j1 < 8; ++j1) {
+    s0[64 * hi + 8 * j1 + lo] = x0[j1];
+    s1[64 * hi + 8 * j1 + lo] = x1[j1];
+  }
+  sync();
+#pragma unroll
+  for (int k0 = 0; k0 < 8; ++k0) {
+    const cd w = tw->tw1[k0][t];
+    x0[k0] = cmulc(s0[64 * k0 + t], w);
+    x1[k0] = cmulc(s1[64 * k0 + t], w);
+  }
+  dft8<-1>(x0);
+  dft8<-1>(x1);
+#pragma unroll
+  for (int m = 1; m < 8; ++m) {
+    x0[m] = cmulc(x0[m], fold_twist(m));
+    x1[m] = cmulc(x1[m], fold_twist(m));
+  }
+}
+
 // ---- rotation and gadget decomposition -----------------------------------------
 // coefficient j of X^abar * P - P for P in shared memory (N words), abar in [0, 2N)
 TFB_HD uint32_t rotated_diff(const uint32_t* poly, int j, int abar) {
@@ -222,48 +316,64 @@ TFB_HD uint32_t digit_field(uint32_t v_plus_offset, int lvl) {
 }
 
 // ---- one CMux step -----------------------------------------------------------------
+// Spectral key layout: one "stage" per (LWE index i, accumulator polynomial p),
+// STAGE_CD complex values laid out [k2][lvl][c][t], prescaled by 1/512, so the
+// MAC of one paired forward transform reads one contiguous 32 KB block.
+constexpr int STAGE_CD = 8 * BK_L * 2 * FFT_THREADS;  // 2048 cd = 32 KB
+TFB_HD size_t stage_offset(int i, int p) { return ((size_t)i * 2 + p) * STAGE_CD; }
+TFB_HD int stage_index(int k2, int lvl, int c, int t) { return ((k2 * BK_L + lvl) * 2 + c) * FFT_THREADS + t; }
+
+// A BkSource hands out the key one stage at a time:
+//   const cd* acquire(i, p)   pointer to the stage (blocks until it is resident)
+//   cd load(q)                one value of it
+//   void release()            this thread is done with the stage
+//   void skip(i)              the CMux of index i is skipped (abar == 0); keeps a
+//                             staged pipeline's bookkeeping in step
+struct GlobalBk {  // plain pointer into the full key (host emulation, key setup checks)
+  const cd* base;
+  TFB_HD const cd* acquire(int i, int p) { return base + stage_offset(i, p); }
+  TFB_HD cd load(const cd* q) const { return *q; }
+  TFB_HD void release() {}
+  TFB_HD void skip(int) {}
+};
+
 // acc: 2 polynomials of N words in shared memory ([0..N) = a, [N..2N) = b).
-// bk : spectral key of this LWE index, laid out [row][k2][c][t] (cd), prescaled by 1/512.
 // Every thread of the 64-thread group calls this; `sync` is the group barrier.
-template <class Sync, class LoadBk>
-TFB_HD void cmux_step(uint32_t* acc, int abar, const cd* bk, int t, const Twiddles* tw, cd* bufA,
-                      cd* bufB, Sync& sync, LoadBk load_bk) {
+// Both gadget levels of one accumulator polynomial are transformed as a pair,
+// then both output polynomials are inverse-transformed as a pair.
+template <class Sync, class BkSource>
+TFB_HD void cmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, const Twiddles* tw, cd* s0, cd* s1,
+                      Sync& sync) {
   cd out0[8], out1[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) out0[k] = out1[k] = cd{0.0, 0.0};
 
 #pragma unroll 1
   for (int p = 0; p < 2; ++p) {
-    uint32_t v[16];
+    cd x0[8], x1[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-      v[m] = rotated_diff(acc + p * RING_N, t + 64 * m, abar) + DECOMP_OFFSET;
-      v[8 + m] = rotated_diff(acc + p * RING_N, t + 64 * m + HALF_N, abar) + DECOMP_OFFSET;
+      const uint32_t vr = rotated_diff(acc + p * RING_N, t + 64 * m, abar) + DECOMP_OFFSET;
+      const uint32_t vi = rotated_diff(acc + p * RING_N, t + 64 * m + HALF_N, abar) + DECOMP_OFFSET;
+      x0[m] = cd{digit_to_double(digit_field(vr, 0)), digit_to_double(digit_field(vi, 0))};
+      x1[m] = cd{digit_to_double(digit_field(vr, 1)), digit_to_double(digit_field(vi, 1))};
     }
+    fft_forward2(x0, x1, t, tw, s0, s1, sync);
+    const cd* stage = bk.acquire(i, p);
 #pragma unroll
-    for (int lvl = 0; lvl < BK_L; ++lvl) {
-      cd x[8];
-#pragma unroll
-      for (int m = 0; m < 8; ++m)
-        x[m] = cd{digit_to_double(digit_field(v[m], lvl)), digit_to_double(digit_field(v[8 + m], lvl))};
-      fft_forward(x, t, tw, bufA, bufB, sync);
-      const cd* row = bk + (size_t)(p * BK_L + lvl) * (8 * 2 * FFT_THREADS);
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) {
-        cmac(out0[k2], x[k2], load_bk(row + (k2 * 2 + 0) * FFT_THREADS + t));
-        cmac(out1[k2], x[k2], load_bk(row + (k2 * 2 + 1) * FFT_THREADS + t));
-      }
+    for (int k2 = 0; k2 < 8; ++k2) {
+      cmac(out0[k2], x0[k2], bk.load(stage + stage_index(k2, 0, 0, t)));
+      cmac(out1[k2], x0[k2], bk.load(stage + stage_index(k2, 0, 1, t)));
+      cmac(out0[k2], x1[k2], bk.load(stage + stage_index(k2, 1, 0, t)));
+      cmac(out1[k2], x1[k2], bk.load(stage + stage_index(k2, 1, 1, t)));
     }
+    bk.release();
   }
-  fft_inverse(out0, t, tw, bufA, bufB, sync);
+  fft_inverse2(out0, out1, t, tw, s0, s1, sync);
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
     acc[t + 64 * m] += round_to_word(out0[m].re);
     acc[t + 64 * m + HALF_N] += round_to_word(out0[m].im);
-  }
-  fft_inverse(out1, t, tw, bufA, bufB, sync);
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
     acc[RING_N + t + 64 * m] += round_to_word(out1[m].re);
     acc[RING_N + t + 64 * m + HALF_N] += round_to_word(out1[m].im);
   }
@@ -290,12 +400,12 @@ TFB_HD int mod_switch(uint32_t a) { return (int)((a + (1u << 20)) >> 21) & (2 * 
 
 // Whole gate bootstrap (without key switch) for one ciphertext by one 64-thread group.
 //   x_row, y_row: pool rows (n mask words then the body)
-//   sm_acc: 2N words, sm_abar: n+1 uint16, bufA/bufB: 512 cd each
+//   sm_acc: 2N words, sm_abar: n+1 uint16, s0/s1: 512 cd each (exchange buffers)
 //   ext: N+1 words out (extracted LWE sample under the ring key)
-template <class Sync, class LoadBk>
+template <class Sync, class BkSource>
 TFB_HD void gate_bootstrap(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu,
-                           const cd* bkf, const Twiddles* tw, uint32_t* sm_acc, uint16_t* sm_abar,
-                           cd* bufA, cd* bufB, uint32_t* ext, int t, Sync& sync, LoadBk load_bk) {
+                           BkSource& bk, const Twiddles* tw, uint32_t* sm_acc, uint16_t* sm_abar,
+                           cd* s0, cd* s1, uint32_t* ext, int t, Sync& sync) {
   int32_t cx, cy, off;
   gate_coeffs(kind, cx, cy, off);
   for (int w = t; w <= n; w += FFT_THREADS) {
@@ -315,9 +425,11 @@ TFB_HD void gate_bootstrap(const uint32_t* x_row, const uint32_t* y_row, int kin
 #pragma unroll 1
   for (int i = 0; i < n; ++i) {
     const int abar = sm_abar[i];
-    if (abar == 0) continue;  // uniform across the group
-    cmux_step(sm_acc, abar, bkf + (size_t)i * (BK_ROWS * 8 * 2 * FFT_THREADS), t, tw, bufA, bufB, sync,
-              load_bk);
+    if (abar == 0) {  // uniform across the group
+      bk.skip(i);
+      continue;
+    }
+    cmux_step(sm_acc, abar, i, bk, t, tw, s0, s1, sync);
   }
   // sample extract at coefficient 0: a'_0 = a_0, a'_j = -a_{N-j}; b' = b_0
   for (int j = t; j < RING_N; j += FFT_THREADS) ext[j] = (j == 0) ? sm_acc[0] : (0u - sm_acc[RING_N - j]);

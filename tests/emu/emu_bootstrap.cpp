@@ -20,9 +20,6 @@ struct BarrierSync {
   pthread_barrier_t* b;
   void operator()() const { pthread_barrier_wait(b); }
 };
-struct PlainLoad {
-  cd operator()(const cd* p) const { return *p; }
-};
 
 void fill_twiddles(Twiddles* tw) {
   const long double pi = 3.141592653589793238462643383279502884L;
@@ -51,7 +48,7 @@ void run_group(F body) {
 
 extern "C" {
 
-// spectral key in the kernel's layout [n][4][8][2][64], prescaled by 1/512
+// spectral key in the kernel's staged layout [n][p][k2][lvl][c][t], prescaled by 1/512
 void emu_bk_transform(const int32_t* bk_raw, int n, double* bkf_out) {
   Twiddles tw;
   fill_twiddles(&tw);
@@ -67,7 +64,8 @@ void emu_bk_transform(const int32_t* bk_raw, int n, double* bkf_out) {
         x[m] = cd{int32_to_double(src[t + 64 * m]), int32_to_double(src[t + 64 * m + HALF_N])};
       fft_forward(x, t, &tw, bufA.data(), bufB.data(), s);
       for (int k2 = 0; k2 < 8; ++k2)
-        bkf[((ir * 8 + k2) * 2 + c) * FFT_THREADS + t] = cd{x[k2].re / HALF_N, x[k2].im / HALF_N};
+        bkf[stage_offset((int)(ir / BK_ROWS), (int)(ir % BK_ROWS) / BK_L) + stage_index(k2, (int)(ir % BK_L), c, t)] =
+            cd{x[k2].re / HALF_N, x[k2].im / HALF_N};
     });
   }
 }
@@ -119,8 +117,9 @@ void emu_gate_bootstrap(const uint32_t* x, const uint32_t* y, const uint8_t* kin
     std::vector<uint32_t> acc(2 * RING_N), ext(EXT_STRIDE);
     std::vector<uint16_t> abar(n + 1);
     run_group([&](int t, BarrierSync& s) {
-      gate_bootstrap(x + g * (n + 1), y + g * (n + 1), (int)kinds[g], n, mu, bkf, &tw, acc.data(), abar.data(),
-                     bufA.data(), bufB.data(), ext.data(), t, s, PlainLoad());
+      GlobalBk bk{bkf};
+      gate_bootstrap(x + g * (n + 1), y + g * (n + 1), (int)kinds[g], n, mu, bk, &tw, acc.data(), abar.data(),
+                     bufA.data(), bufB.data(), ext.data(), t, s);
     });
     for (int j = 0; j <= RING_N; ++j) ext_out[g * (RING_N + 1) + j] = ext[j];
   }
