@@ -46,7 +46,7 @@ struct tfb_ctx {
   int64_t host_cap = 0;
   int64_t launches = 0;
   int sm_count = 148;
-  int force_kernel = 0;        // 0 auto, 1 = K1a (one ciphertext per CTA), 2 = K1b (ring)
+  int force_kernel = 0;        // 0 auto, 1 = K1a (one ciphertext per CTA), 2 = K1b (ring), 3 = K1c (wide)
   std::string err;
 };
 
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(FFT_THREADS, TFB_K1_MIN_BLOCKS) k_gate_bootstr
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
     const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
     const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
   cd* s0 = reinterpret_cast<cd*>(smem + sizeof(Twiddles));
   cd* s1 = s0 + HALF_N;
@@ -144,6 +144,45 @@ __global__ void __launch_bounds__(FFT_THREADS, TFB_K1_MIN_BLOCKS) k_gate_bootstr
   LdgBk bk{bkf};
   gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, ext + g * EXT_STRIDE,
                  (int)threadIdx.x, sync);
+}
+
+// ------------------------------------------------------------------------------------
+// K1c: latency variant, ONE ciphertext per 256-thread CTA (gate_bootstrap_wide): the four
+//      digit polynomials of a CMux are transformed concurrently by four 64-thread groups.
+//      Used when a launch has fewer gates than SMs (ripple-carry adders, multiplier trees).
+// ------------------------------------------------------------------------------------
+constexpr int K1C_THREADS = 4 * FFT_THREADS;
+// dynamic smem: twiddles | xbuf 4x2x512 cd | red 4x2x512 cd | acc | abar
+__host__ __device__ constexpr int k1c_smem(int n) {
+  return (int)sizeof(Twiddles) + 16 * HALF_N * (int)sizeof(cd) + 2 * RING_N * (int)sizeof(uint32_t) +
+         ((n + 1) * 2 + 15) / 16 * 16;
+}
+struct LdgLoad {
+  __device__ __forceinline__ cd operator()(const cd* q) const {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(q));
+    return cd{v.x, v.y};
+  }
+};
+
+__global__ void __launch_bounds__(K1C_THREADS, 1) k_gate_bootstrap_wide(
+    const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
+    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
+    const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
+  cd* xbuf = reinterpret_cast<cd*>(smem + sizeof(Twiddles));
+  cd* red = xbuf + 8 * HALF_N;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(red + 8 * HALF_N);
+  uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
+  for (int i = threadIdx.x; i < (int)(sizeof(Twiddles) / sizeof(cd)); i += K1C_THREADS)
+    reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
+  const int64_t g = blockIdx.x;
+  const uint32_t* xr = pool + (int64_t)x_rows[g] * ROW_STRIDE;
+  const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
+  GroupSync gsync{(int)(threadIdx.x / FFT_THREADS) + 1};
+  BlockSync csync;
+  gate_bootstrap_wide(xr, yr, (int)kinds[g], n, mu, bkf, tw, acc, abar, xbuf, red, ext + g * EXT_STRIDE,
+                      (int)threadIdx.x, gsync, csync, LdgLoad());
 }
 
 // ------------------------------------------------------------------------------------
@@ -259,7 +298,9 @@ __global__ void __launch_bounds__(KS_THREADS) k_key_switch(const uint32_t* __res
                                                            const int32_t* __restrict__ ksk,
                                                            uint32_t* __restrict__ pool,
                                                            const int32_t* __restrict__ out_rows, int n,
-                                                           int64_t k) {
+                                                           int64_t k, int i_per_cta) {
+  // gridDim.y > 1: the ring coefficients are split over blockIdx.y and the partial sums are
+  // combined with integer atomics into rows zeroed by k_rows_zero (small launches: latency).
   __shared__ __align__(16) int32_t digits[KS_CHUNK_R][KS_CT];
   const int tid = threadIdx.x;
   const int64_t c0 = (int64_t)blockIdx.x * KS_CT;
@@ -268,7 +309,8 @@ __global__ void __launch_bounds__(KS_THREADS) k_key_switch(const uint32_t* __res
   for (int c = 0; c < KS_CT; ++c) acc0[c] = acc1[c] = 0;
   const uint32_t bias = ks_bias();
 
-  for (int i0 = 0; i0 < RING_N; i0 += KS_CHUNK_I) {
+  const int i_begin = blockIdx.y * i_per_cta, i_end = i_begin + i_per_cta;
+  for (int i0 = i_begin; i0 < i_end; i0 += KS_CHUNK_I) {
     __syncthreads();
     // digits of ext[c][i0 .. i0+16) for the tile's ciphertexts: 512 words, 2 per thread
     for (int e = tid; e < KS_CT * KS_CHUNK_I; e += KS_THREADS) {
@@ -301,14 +343,27 @@ __global__ void __launch_bounds__(KS_THREADS) k_key_switch(const uint32_t* __res
       }
     }
   }
+  const bool split = gridDim.y > 1;
 #pragma unroll
   for (int c = 0; c < KS_CT; ++c) {
     if (c0 + c >= k) break;
     uint32_t* row = pool + (int64_t)out_rows[c0 + c] * ROW_STRIDE;
-    const uint32_t body = ext[(c0 + c) * EXT_STRIDE + RING_N];
-    row[tid] = (tid == n ? body : 0u) - (uint32_t)acc0[c];
-    row[tid + KS_THREADS] = (tid + KS_THREADS == n ? body : 0u) - (uint32_t)acc1[c];
+    const uint32_t body = (blockIdx.y == 0) ? ext[(c0 + c) * EXT_STRIDE + RING_N] : 0u;
+    const uint32_t v0 = (tid == n ? body : 0u) - (uint32_t)acc0[c];
+    const uint32_t v1 = (tid + KS_THREADS == n ? body : 0u) - (uint32_t)acc1[c];
+    if (split) {
+      atomicAdd(row + tid, v0);
+      atomicAdd(row + tid + KS_THREADS, v1);
+    } else {
+      row[tid] = v0;
+      row[tid + KS_THREADS] = v1;
+    }
   }
+}
+
+__global__ void k_rows_zero(uint32_t* __restrict__ pool, const int32_t* __restrict__ rows) {
+  uint32_t* dst = pool + (int64_t)rows[blockIdx.x] * ROW_STRIDE;
+  for (int c = threadIdx.x; c < ROW_STRIDE; c += blockDim.x) dst[c] = 0u;
 }
 
 // ------------------------------------------------------------------------------------
@@ -465,6 +520,8 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gate_bootstrap_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              K1B_HEADER + K1B_GROUPS * group_smem(p->n));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gate_bootstrap_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, k1c_smem(p->n));
   if (e == cudaSuccess) {
     int sms = 0;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -529,8 +586,15 @@ static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* ki
   const int n = ctx->p.n;
   // K1b keeps K1B_GROUPS ciphertexts on one SM; below one full wave of such CTAs the
   // one-ciphertext-per-CTA kernel spreads the launch over more SMs and wins.
-  const bool ring = ctx->force_kernel ? ctx->force_kernel == 2 : k >= (int64_t)ctx->sm_count * K1B_GROUPS;
-  if (ring) {
+  // K1c: up to two waves of one-gate-per-SM CTAs (4 groups per gate) beat six gates per SM on latency.
+  // K1b keeps K1B_GROUPS ciphertexts on one SM; below one full wave of such CTAs the
+  // one-ciphertext-per-CTA kernel K1a spreads the launch over more SMs and wins.
+  int which = ctx->force_kernel;
+  if (!which) which = k <= 2 * ctx->sm_count ? 3 : (k >= (int64_t)ctx->sm_count * K1B_GROUPS ? 2 : 1);
+  if (which == 3) {
+    k_gate_bootstrap_wide<<<(unsigned)k, K1C_THREADS, k1c_smem(n), st>>>(
+        (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
+  } else if (which == 2) {
     const unsigned grid = (unsigned)((k + K1B_GROUPS - 1) / K1B_GROUPS);
     k_gate_bootstrap_ring<<<grid, K1B_THREADS, K1B_HEADER + K1B_GROUPS * group_smem(n), st>>>(
         (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext, k);
@@ -545,8 +609,16 @@ static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* ki
 
 static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, const int32_t* out_rows,
                              int64_t k, cudaStream_t st) {
-  const unsigned grid = (unsigned)((k + KS_CT - 1) / KS_CT);
-  k_key_switch<<<grid, KS_THREADS, 0, st>>>(ext, ctx->d_ksk, (uint32_t*)pool, out_rows, ctx->p.n, k);
+  const unsigned tiles = (unsigned)((k + KS_CT - 1) / KS_CT);
+  // small launches: split the 1024 ring coefficients over up to 64 CTAs per tile to fill the chip
+  unsigned split = 1;
+  while (split < RING_N / KS_CHUNK_I && tiles * split < 2u * (unsigned)ctx->sm_count) split *= 2;
+  if (split > 1) {
+    k_rows_zero<<<(unsigned)k, 128, 0, st>>>((uint32_t*)pool, out_rows);
+    ctx->launches += 1;
+  }
+  k_key_switch<<<dim3(tiles, split), KS_THREADS, 0, st>>>(ext, ctx->d_ksk, (uint32_t*)pool, out_rows, ctx->p.n, k,
+                                                         RING_N / (int)split);
   ctx->launches += 1;
   TFB_CUDA(ctx, cudaGetLastError());
   return TFB_OK;

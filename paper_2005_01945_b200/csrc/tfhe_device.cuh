@@ -341,34 +341,48 @@ struct GlobalBk {  // plain pointer into the full key (host emulation, key setup
 // Every thread of the 64-thread group calls this; `sync` is the group barrier.
 // Both gadget levels of one accumulator polynomial are transformed as a pair,
 // then both output polynomials are inverse-transformed as a pair.
+// One accumulator polynomial p of a CMux: rotate-and-subtract, decompose, paired
+// forward transform, MAC against stage (i, p).  P == 0 initialises the output
+// accumulators instead of adding to them, so they are not live (64 registers)
+// during the first paired transform.
+template <int P, class Sync, class BkSource>
+TFB_HD void cmux_half(cd* out0, cd* out1, const uint32_t* acc, int abar, int i, BkSource& bk, int t,
+                      const Twiddles* tw, cd* s0, cd* s1, Sync& sync) {
+  cd x0[8], x1[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const uint32_t vr = rotated_diff(acc + P * RING_N, t + 64 * m, abar) + DECOMP_OFFSET;
+    const uint32_t vi = rotated_diff(acc + P * RING_N, t + 64 * m + HALF_N, abar) + DECOMP_OFFSET;
+    x0[m] = cd{digit_to_double(digit_field(vr, 0)), digit_to_double(digit_field(vi, 0))};
+    x1[m] = cd{digit_to_double(digit_field(vr, 1)), digit_to_double(digit_field(vi, 1))};
+  }
+  fft_forward2(x0, x1, t, tw, s0, s1, sync);
+  const cd* stage = bk.acquire(i, P);
+#pragma unroll
+  for (int k2 = 0; k2 < 8; ++k2) {
+    if (P == 0) {
+      out0[k2] = cmul(x0[k2], bk.load(stage + stage_index(k2, 0, 0, t)));
+      out1[k2] = cmul(x0[k2], bk.load(stage + stage_index(k2, 0, 1, t)));
+    } else {
+      cmac(out0[k2], x0[k2], bk.load(stage + stage_index(k2, 0, 0, t)));
+      cmac(out1[k2], x0[k2], bk.load(stage + stage_index(k2, 0, 1, t)));
+    }
+    cmac(out0[k2], x1[k2], bk.load(stage + stage_index(k2, 1, 0, t)));
+    cmac(out1[k2], x1[k2], bk.load(stage + stage_index(k2, 1, 1, t)));
+  }
+  bk.release();
+}
+
+// acc: 2 polynomials of N words in shared memory ([0..N) = a, [N..2N) = b).
+// Every thread of the 64-thread group calls this; `sync` is the group barrier.
+// Both gadget levels of one accumulator polynomial are transformed as a pair,
+// then both output polynomials are inverse-transformed as a pair.
 template <class Sync, class BkSource>
 TFB_HD void cmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, const Twiddles* tw, cd* s0, cd* s1,
                       Sync& sync) {
   cd out0[8], out1[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) out0[k] = out1[k] = cd{0.0, 0.0};
-
-#pragma unroll 1
-  for (int p = 0; p < 2; ++p) {
-    cd x0[8], x1[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      const uint32_t vr = rotated_diff(acc + p * RING_N, t + 64 * m, abar) + DECOMP_OFFSET;
-      const uint32_t vi = rotated_diff(acc + p * RING_N, t + 64 * m + HALF_N, abar) + DECOMP_OFFSET;
-      x0[m] = cd{digit_to_double(digit_field(vr, 0)), digit_to_double(digit_field(vi, 0))};
-      x1[m] = cd{digit_to_double(digit_field(vr, 1)), digit_to_double(digit_field(vi, 1))};
-    }
-    fft_forward2(x0, x1, t, tw, s0, s1, sync);
-    const cd* stage = bk.acquire(i, p);
-#pragma unroll
-    for (int k2 = 0; k2 < 8; ++k2) {
-      cmac(out0[k2], x0[k2], bk.load(stage + stage_index(k2, 0, 0, t)));
-      cmac(out1[k2], x0[k2], bk.load(stage + stage_index(k2, 0, 1, t)));
-      cmac(out0[k2], x1[k2], bk.load(stage + stage_index(k2, 1, 0, t)));
-      cmac(out1[k2], x1[k2], bk.load(stage + stage_index(k2, 1, 1, t)));
-    }
-    bk.release();
-  }
+  cmux_half<0>(out0, out1, acc, abar, i, bk, t, tw, s0, s1, sync);
+  cmux_half<1>(out0, out1, acc, abar, i, bk, t, tw, s0, s1, sync);
   fft_inverse2(out0, out1, t, tw, s0, s1, sync);
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
@@ -398,6 +412,34 @@ TFB_HD void gate_coeffs(int kind, int32_t& cx, int32_t& cy, int32_t& off) {
 // round(a * 2N / 2^32) mod 2N
 TFB_HD int mod_switch(uint32_t a) { return (int)((a + (1u << 20)) >> 21) & (2 * RING_N - 1); }
 
+// Gate linear form + mod switch + accumulator initialisation, by `nthreads` threads.
+//   ACC = (0, X^{2N - bbar} * testvector), testvector = mu * (1 + X + ... + X^{N-1})
+template <class Sync>
+TFB_HD void bootstrap_prologue(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu,
+                               uint32_t* sm_acc, uint16_t* sm_abar, int tid, int nthreads, Sync& sync) {
+  int32_t cx, cy, off;
+  gate_coeffs(kind, cx, cy, off);
+  for (int w = tid; w <= n; w += nthreads) {
+    uint32_t v = (uint32_t)cx * x_row[w] + (uint32_t)cy * y_row[w];
+    if (w == n) v += (uint32_t)off * mu;
+    sm_abar[w] = (uint16_t)mod_switch(v);
+  }
+  sync();
+  const int bbar = sm_abar[n];
+  for (int j = tid; j < RING_N; j += nthreads) {
+    sm_acc[j] = 0;
+    const int src = (j + bbar) & (2 * RING_N - 1);  // j - (2N - bbar) mod 2N
+    sm_acc[RING_N + j] = (src < RING_N) ? mu : (0u - mu);
+  }
+  sync();
+}
+
+// sample extract at coefficient 0: a'_0 = a_0, a'_j = -a_{N-j}; b' = b_0
+TFB_HD void bootstrap_extract(const uint32_t* sm_acc, uint32_t* ext, int tid, int nthreads) {
+  for (int j = tid; j < RING_N; j += nthreads) ext[j] = (j == 0) ? sm_acc[0] : (0u - sm_acc[RING_N - j]);
+  if (tid == 0) ext[RING_N] = sm_acc[RING_N];
+}
+
 // Whole gate bootstrap (without key switch) for one ciphertext by one 64-thread group.
 //   x_row, y_row: pool rows (n mask words then the body)
 //   sm_acc: 2N words, sm_abar: n+1 uint16, s0/s1: 512 cd each (exchange buffers)
@@ -406,22 +448,7 @@ template <class Sync, class BkSource>
 TFB_HD void gate_bootstrap(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu,
                            BkSource& bk, const Twiddles* tw, uint32_t* sm_acc, uint16_t* sm_abar,
                            cd* s0, cd* s1, uint32_t* ext, int t, Sync& sync) {
-  int32_t cx, cy, off;
-  gate_coeffs(kind, cx, cy, off);
-  for (int w = t; w <= n; w += FFT_THREADS) {
-    uint32_t v = (uint32_t)cx * x_row[w] + (uint32_t)cy * y_row[w];
-    if (w == n) v += (uint32_t)off * mu;
-    sm_abar[w] = (uint16_t)mod_switch(v);
-  }
-  sync();
-  // ACC = (0, X^{2N - bbar} * testvector), testvector = mu * (1 + X + ... + X^{N-1})
-  const int bbar = sm_abar[n];
-  for (int j = t; j < RING_N; j += FFT_THREADS) {
-    sm_acc[j] = 0;
-    const int src = (j + bbar) & (2 * RING_N - 1);  // j - (2N - bbar) mod 2N
-    sm_acc[RING_N + j] = (src < RING_N) ? mu : (0u - mu);
-  }
-  sync();
+  bootstrap_prologue(x_row, y_row, kind, n, mu, sm_acc, sm_abar, t, FFT_THREADS, sync);
 #pragma unroll 1
   for (int i = 0; i < n; ++i) {
     const int abar = sm_abar[i];
@@ -431,9 +458,70 @@ TFB_HD void gate_bootstrap(const uint32_t* x_row, const uint32_t* y_row, int kin
     }
     cmux_step(sm_acc, abar, i, bk, t, tw, s0, s1, sync);
   }
-  // sample extract at coefficient 0: a'_0 = a_0, a'_j = -a_{N-j}; b' = b_0
-  for (int j = t; j < RING_N; j += FFT_THREADS) ext[j] = (j == 0) ? sm_acc[0] : (0u - sm_acc[RING_N - j]);
-  if (t == 0) ext[RING_N] = sm_acc[RING_N];
+  bootstrap_extract(sm_acc, ext, t, FFT_THREADS);
+}
+
+// Latency-oriented variant: ONE ciphertext by FOUR 64-thread groups (256 threads).
+// Group q = 2p + lvl transforms digit polynomial (p, lvl) on its own, multiplies it
+// with its share of key stage (i, p) -- prefetched into registers before the
+// transform -- and the four partial products are summed through shared memory;
+// groups 0 and 1 then inverse-transform output polynomials 0 and 1.  The critical
+// path per CMux is one forward + one inverse transform instead of six.
+//   xbuf: 4 groups x 2 exchange buffers x 512 cd;  red: 4 groups x 2 components x 512 cd
+template <class GroupSync, class CtaSync, class LoadBk>
+TFB_HD void gate_bootstrap_wide(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu,
+                                const cd* bkf, const Twiddles* tw, uint32_t* sm_acc, uint16_t* sm_abar,
+                                cd* xbuf, cd* red, uint32_t* ext, int tid, GroupSync& gsync, CtaSync& csync,
+                                LoadBk load) {
+  constexpr int WIDE = 4 * FFT_THREADS;
+  const int q = tid / FFT_THREADS, t = tid % FFT_THREADS;
+  const int p = q / BK_L, lvl = q % BK_L;
+  cd* bufA = xbuf + (size_t)q * 2 * HALF_N;
+  cd* bufB = bufA + HALF_N;
+  bootstrap_prologue(x_row, y_row, kind, n, mu, sm_acc, sm_abar, tid, WIDE, csync);
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    const int abar = sm_abar[i];
+    if (abar == 0) continue;  // uniform across the CTA
+    const cd* stage = bkf + stage_offset(i, p);
+    cd b0[8], b1[8];
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) {
+      b0[k2] = load(stage + stage_index(k2, lvl, 0, t));
+      b1[k2] = load(stage + stage_index(k2, lvl, 1, t));
+    }
+    cd x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const uint32_t vr = rotated_diff(sm_acc + p * RING_N, t + 64 * m, abar) + DECOMP_OFFSET;
+      const uint32_t vi = rotated_diff(sm_acc + p * RING_N, t + 64 * m + HALF_N, abar) + DECOMP_OFFSET;
+      x[m] = cd{digit_to_double(digit_field(vr, lvl)), digit_to_double(digit_field(vi, lvl))};
+    }
+    fft_forward(x, t, tw, bufA, bufB, gsync);
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) {
+      red[((q * 2 + 0) * 8 + k2) * FFT_THREADS + t] = cmul(x[k2], b0[k2]);
+      red[((q * 2 + 1) * 8 + k2) * FFT_THREADS + t] = cmul(x[k2], b1[k2]);
+    }
+    csync();
+    if (q < 2) {  // output polynomial c = q
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) {
+        cd s = red[((0 * 2 + q) * 8 + k2) * FFT_THREADS + t];
+        s = cadd(s, red[((1 * 2 + q) * 8 + k2) * FFT_THREADS + t]);
+        s = cadd(s, red[((2 * 2 + q) * 8 + k2) * FFT_THREADS + t]);
+        x[k2] = cadd(s, red[((3 * 2 + q) * 8 + k2) * FFT_THREADS + t]);
+      }
+      fft_inverse(x, t, tw, bufA, bufB, gsync);
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        sm_acc[q * RING_N + t + 64 * m] += round_to_word(x[m].re);
+        sm_acc[q * RING_N + t + 64 * m + HALF_N] += round_to_word(x[m].im);
+      }
+    }
+    csync();
+  }
+  bootstrap_extract(sm_acc, ext, tid, WIDE);
 }
 
 // ---- key switch ---------------------------------------------------------------------------

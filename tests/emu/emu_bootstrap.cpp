@@ -125,6 +125,35 @@ void emu_gate_bootstrap(const uint32_t* x, const uint32_t* y, const uint8_t* kin
   }
 }
 
+// K1c (wide / latency variant): 256 host threads per ciphertext, 4 group barriers + 1 CTA barrier
+void emu_gate_bootstrap_wide(const uint32_t* x, const uint32_t* y, const uint8_t* kinds, int64_t k, int n,
+                             uint32_t mu, const double* bkf_in, uint32_t* ext_out) {
+  Twiddles tw;
+  fill_twiddles(&tw);
+  const cd* bkf = reinterpret_cast<const cd*>(bkf_in);
+  constexpr int WIDE = 4 * FFT_THREADS;
+  for (int64_t g = 0; g < k; ++g) {
+    std::vector<cd> xbuf(8 * HALF_N), red(8 * HALF_N);
+    std::vector<uint32_t> acc(2 * RING_N), ext(EXT_STRIDE);
+    std::vector<uint16_t> abar(n + 1);
+    pthread_barrier_t cta, grp[4];
+    pthread_barrier_init(&cta, nullptr, WIDE);
+    for (auto& b : grp) pthread_barrier_init(&b, nullptr, FFT_THREADS);
+    std::vector<std::thread> th;
+    for (int tid = 0; tid < WIDE; ++tid)
+      th.emplace_back([&, tid] {
+        BarrierSync gs{&grp[tid / FFT_THREADS]}, cs{&cta};
+        gate_bootstrap_wide(x + g * (n + 1), y + g * (n + 1), (int)kinds[g], n, mu, bkf, &tw, acc.data(),
+                            abar.data(), xbuf.data(), red.data(), ext.data(), tid, gs, cs,
+                            [](const cd* q) { return *q; });
+      });
+    for (auto& t : th) t.join();
+    pthread_barrier_destroy(&cta);
+    for (auto& b : grp) pthread_barrier_destroy(&b);
+    for (int j = 0; j <= RING_N; ++j) ext_out[g * (RING_N + 1) + j] = ext[j];
+  }
+}
+
 // key-switch digits exactly as K2 derives them: digits_out[N][KS_T]
 void emu_ks_digits(const uint32_t* ext, int32_t* digits_out) {
   const uint32_t bias = ks_bias();

@@ -169,6 +169,11 @@ def test_kernel_arithmetic_on_host_threads_matches_oracle(emu_lib, key):
     emu_lib.emu_gate_bootstrap(vp(xs.ctypes.data), vp(ys.ctypes.data), vp(kinds.ctypes.data), ctypes.c_int64(K), n,
                                ctypes.c_uint32(p.mu.word), vp(bkf.ctypes.data), vp(got.ctypes.data))
     assert np.array_equal(got, ext)
+    # the latency variant (one ciphertext over four thread groups) must produce the same words
+    wide = np.empty((K, 1025), dtype=np.uint32)
+    emu_lib.emu_gate_bootstrap_wide(vp(xs.ctypes.data), vp(ys.ctypes.data), vp(kinds.ctypes.data), ctypes.c_int64(K),
+                                    n, ctypes.c_uint32(p.mu.word), vp(bkf.ctypes.data), vp(wide.ctypes.data))
+    assert np.array_equal(wide, ext)
     # K2's digit extraction against the oracle's key switch
     digits = np.empty((1024, 8), dtype=np.int32)
     emu_lib.emu_ks_digits(vp(ext[0].ctypes.data), vp(digits.ctypes.data))
