@@ -213,7 +213,8 @@ def run_b200(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    distributed = "RANK" in os.environ and "WORLD_SIZE" in os.environ  # launched by torch.distributed.run
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -224,7 +225,7 @@ def run_b200(args) -> None:
     ctx = _cabi.Context(local, n, key.params.mu.word, ring)
     stream = torch.cuda.current_stream(dev).cuda_stream
     # evaluation keys: generated on rank 0, broadcast raw over NCCL, transformed on every GPU (kernel K3)
-    if world > 1:
+    if distributed:
         bk_t = torch.empty((n, ring.rows, 2, ring.N), dtype=torch.int32, device=dev)
         ksk_t = torch.empty((ring.N, ring.ks_t, n + 1), dtype=torch.int32, device=dev)
         if rank == 0:
@@ -253,7 +254,7 @@ def run_b200(args) -> None:
                  k, stream)
 
     def fence():
-        if world > 1:
+        if distributed:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
@@ -266,7 +267,7 @@ def run_b200(args) -> None:
         e1.record()
         fence()
         ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
+        if distributed:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item())
 
@@ -283,7 +284,7 @@ def run_b200(args) -> None:
     ctx.call("tfb_rows_phase", pool.data_ptr(), orow.data_ptr(), key_bits_t.data_ptr(), ph.data_ptr(), k, stream)
     phase = ph.cpu().numpy().view(np.uint32)
     correct = bool(np.array_equal(((phase > 0) & (phase < 2**31)).astype(int), 1 - (bits[0] & bits[1])))
-    if world > 1:
+    if distributed:
         flag = torch.tensor([int(correct)], device=dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         correct = bool(flag.item())
@@ -318,7 +319,7 @@ def run_b200(args) -> None:
         e2e_step()
     fence()
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = world * k * e2e_steps / float(e2e_s.item())
     out_words = hout.numpy().view(np.uint32)
@@ -326,7 +327,7 @@ def run_b200(args) -> None:
     e2e_ok = bool(np.array_equal(((e2e_phase > 0) & (e2e_phase < 2**31)).astype(int), 1 - (bits[0] & bits[1])))
 
     if rank != 0:
-        if world > 1:
+        if distributed:
             dist.destroy_process_group()
         return
 
@@ -348,7 +349,7 @@ def run_b200(args) -> None:
         "gpu_launches": int(gpu_launches),
         "correct": correct,
         "roofline": {
-            "kernel": "k_gate_bootstrap (fused linear form + blind rotation + sample extract)",
+            "kernel": "k_gate_bootstrap_ring (fused linear form + blind rotation + sample extract)",
             "bound": "fp64", "achieved": k1_tflops, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
             "frac": k1_tflops / peaks["fp64_tflops"], "traffic": traffic,
             "flop_per_gate": FLOP_PER_GATE, "ms_per_launch": k1_ms, "share_of_step": k1_ms / (total_ms / args.steps),
@@ -372,7 +373,7 @@ def run_b200(args) -> None:
             "sample": "256 NAND gates, oracle/tfhe_gate_oracle.c double-FFT path (real TFHE bootstrap + key switch); "
                       "NOT the reference -- the like-for-like CPU comparator", "correct": real_ok}
     print(json.dumps(line))
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

@@ -141,9 +141,14 @@ TFB_HD void dft8(cd* x) {
 //               per-thread part exp(i pi t / N) of the negacyclic twist folded in)
 // tw2[k][a]   = exp(2 pi i a k / 64)          (pass-2 twiddle)
 // Both are stored [register index][thread] so a warp reads consecutive words.
+// g[t] = exp(2 pi i t / 512): ratio tw1[k+1][t] / tw1[k][t].  The paired transforms load only
+// tw1[0][t], g[t] and tw2[1][lo] and rebuild the other twiddles by repeated multiplication:
+// the kernel is bound by the shared-memory data pipe, not by FP64, so 13 complex
+// multiplications are cheaper than 13 16-byte loads per pass pair.
 struct Twiddles {
   cd tw1[8][FFT_THREADS];
   cd tw2[8][8];
+  cd g[FFT_THREADS];
 };
 
 // exp(i pi m / 16): the exp(i pi 64 m / N) part of the negacyclic twist, which
@@ -224,11 +229,15 @@ TFB_HD void fft_forward2(cd* x0, cd* x1, int t, const Twiddles* tw, cd* s0, cd* 
   dft8<1>(x0);
   dft8<1>(x1);
   sync();  // previous readers of s0/s1 are done
+  {
+    cd w = tw->tw1[0][t];
+    const cd g = tw->g[t];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const cd w = tw->tw1[k][t];
-    s0[64 * k + t] = cmul(x0[k], w);
-    s1[64 * k + t] = cmul(x1[k], w);
+    for (int k = 0; k < 8; ++k) {
+      s0[64 * k + t] = cmul(x0[k], w);
+      s1[64 * k + t] = cmul(x1[k], w);
+      if (k < 7) w = cmul(w, g);
+    }
   }
   sync();
   const int hi = t >> 3, lo = t & 7;
@@ -242,11 +251,15 @@ TFB_HD void fft_forward2(cd* x0, cd* x1, int t, const Twiddles* tw, cd* s0, cd* 
   sync();
   s0[64 * hi + lo] = x0[0];
   s1[64 * hi + lo] = x1[0];
+  {
+    const cd v = tw->tw2[1][lo];
+    cd w = v;
 #pragma unroll
-  for (int k = 1; k < 8; ++k) {
-    const cd w = tw->tw2[k][lo];
-    s0[64 * hi + 8 * k + (lo ^ k)] = cmul(x0[k], w);
-    s1[64 * hi + 8 * k + (lo ^ k)] = cmul(x1[k], w);
+    for (int k = 1; k < 8; ++k) {
+      s0[64 * hi + 8 * k + (lo ^ k)] = cmul(x0[k], w);
+      s1[64 * hi + 8 * k + (lo ^ k)] = cmul(x1[k], w);
+      if (k < 7) w = cmul(w, v);
+    }
   }
   sync();
 #pragma unroll
@@ -266,11 +279,15 @@ TFB_HD void fft_inverse2(cd* x0, cd* x1, int t, const Twiddles* tw, cd* s0, cd* 
   sync();
   s0[64 * hi + 8 * lo + lo] = x0[0];
   s1[64 * hi + 8 * lo + lo] = x1[0];
+  {
+    const cd v = tw->tw2[1][lo];
+    cd w = v;
 #pragma unroll
-  for (int j0 = 1; j0 < 8; ++j0) {
-    const cd w = tw->tw2[j0][lo];
-    s0[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x0[j0], w);
-    s1[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x1[j0], w);
+    for (int j0 = 1; j0 < 8; ++j0) {
+      s0[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x0[j0], w);
+      s1[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x1[j0], w);
+      if (j0 < 7) w = cmul(w, v);
+    }
   }
   sync();
 #pragma unroll
@@ -287,11 +304,15 @@ TFB_HD void fft_inverse2(cd* x0, cd* x1, int t, const Twiddles* tw, cd* s0, cd* 
     s1[64 * hi + 8 * j1 + lo] = x1[j1];
   }
   sync();
+  {
+    cd w = tw->tw1[0][t];
+    const cd g = tw->g[t];
 #pragma unroll
-  for (int k0 = 0; k0 < 8; ++k0) {
-    const cd w = tw->tw1[k0][t];
-    x0[k0] = cmulc(s0[64 * k0 + t], w);
-    x1[k0] = cmulc(s1[64 * k0 + t], w);
+    for (int k0 = 0; k0 < 8; ++k0) {
+      x0[k0] = cmulc(s0[64 * k0 + t], w);
+      x1[k0] = cmulc(s1[64 * k0 + t], w);
+      if (k0 < 7) w = cmul(w, g);
+    }
   }
   dft8<-1>(x0);
   dft8<-1>(x1);

@@ -33,6 +33,10 @@ void fill_twiddles(Twiddles* tw) {
       const long double ang = 2.0L * pi * (long double)(a * k) / 64.0L;
       tw->tw2[k][a] = cd{(double)cosl(ang), (double)sinl(ang)};
     }
+  for (int t = 0; t < FFT_THREADS; ++t) {
+    const long double ang = 2.0L * pi * (long double)t / (long double)HALF_N;
+    tw->g[t] = cd{(double)cosl(ang), (double)sinl(ang)};
+  }
 }
 
 template <class F>
