@@ -215,12 +215,25 @@ TFB_HD void fft_inverse(cd* x, int t, const Twiddles* tw, cd* bufA, cd* bufB, Sy
 
 // ---- paired transforms --------------------------------------------------------
 // Two independent transforms advanced in lock step by the same 64 threads: every
-// twiddle is loaded once and used twice, the barrier count per transform halves
-// and each thread carries twice the independent FP64 work between barriers.
-// s0/s1 are the exchange buffers of the two transforms (512 cd each); both
-// exchanges of a transform reuse its buffer, hence the barrier after each read.
-template <class Sync>
+// twiddle is loaded once and used twice and each thread carries twice the
+// independent FP64 work between barriers.  s0/s1 are the exchange buffers of the
+// two transforms (512 cd each).
+//
+// In-place exchanges.  Every exchange is a permutation of the 512 slots (each slot
+// is read by exactly one thread), and a thread always writes its 8 new values into
+// the 8 slots it read last.  No write can then race with another thread's read, so
+// only the read-after-write barrier of each exchange remains: 2 per transform pair.
+// With slot(a,b,c) = 64a + 8b + (a^b^c) the layouts of consecutive transforms are
+// digit rotations of one another; a CMux runs forward (PHASE 0), forward (PHASE 1),
+// inverse (PHASE 2) and the barrier that ends the CMux closes the cycle.  The XOR
+// term makes every access conflict-free: across the 8 threads of a quarter warp
+// exactly one digit varies.
+TFB_HD int xslot(int a, int b, int c) { return 64 * a + 8 * b + (a ^ b ^ c); }
+
+template <int PHASE, class Sync>
 TFB_HD void fft_forward2(cd* x0, cd* x1, int t, const Twiddles* tw, cd* s0, cd* s1, Sync& sync) {
+  static_assert(PHASE == 0 || PHASE == 1, "forward transforms are the first two of a CMux");
+  const int hi = t >> 3, lo = t & 7;
 #pragma unroll
   for (int m = 1; m < 8; ++m) {
     x0[m] = cmul(x0[m], fold_twist(m));
@@ -228,89 +241,95 @@ TFB_HD void fft_forward2(cd* x0, cd* x1, int t, const Twiddles* tw, cd* s0, cd* 
   }
   dft8<1>(x0);
   dft8<1>(x1);
-  sync();  // previous readers of s0/s1 are done
   {
     cd w = tw->tw1[0][t];
     const cd g = tw->g[t];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      s0[64 * k + t] = cmul(x0[k], w);
-      s1[64 * k + t] = cmul(x1[k], w);
+    for (int k = 0; k < 8; ++k) {  // value k of thread (hi, lo)
+      const int a = PHASE == 0 ? xslot(hi, lo, k) : xslot(lo, k, hi);
+      s0[a] = cmul(x0[k], w);
+      s1[a] = cmul(x1[k], w);
       if (k < 7) w = cmul(w, g);
     }
   }
   sync();
-  const int hi = t >> 3, lo = t & 7;
 #pragma unroll
-  for (int j1 = 0; j1 < 8; ++j1) {
-    x0[j1] = s0[64 * hi + 8 * j1 + lo];
-    x1[j1] = s1[64 * hi + 8 * j1 + lo];
+  for (int j = 0; j < 8; ++j) {  // input j1 = j: value hi of thread (j, lo); pass-2 output j goes back to the same slot
+    const int a = PHASE == 0 ? xslot(j, lo, hi) : xslot(lo, hi, j);
+    x0[j] = s0[a];
+    x1[j] = s1[a];
   }
   dft8<1>(x0);
   dft8<1>(x1);
-  sync();
-  s0[64 * hi + lo] = x0[0];
-  s1[64 * hi + lo] = x1[0];
   {
     const cd v = tw->tw2[1][lo];
     cd w = v;
+    const int a0 = PHASE == 0 ? xslot(0, lo, hi) : xslot(lo, hi, 0);
+    s0[a0] = x0[0];
+    s1[a0] = x1[0];
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
-      s0[64 * hi + 8 * k + (lo ^ k)] = cmul(x0[k], w);
-      s1[64 * hi + 8 * k + (lo ^ k)] = cmul(x1[k], w);
+      const int a = PHASE == 0 ? xslot(k, lo, hi) : xslot(lo, hi, k);
+      s0[a] = cmul(x0[k], w);
+      s1[a] = cmul(x1[k], w);
       if (k < 7) w = cmul(w, v);
     }
   }
   sync();
 #pragma unroll
-  for (int j0 = 0; j0 < 8; ++j0) {
-    x0[j0] = s0[64 * hi + 8 * lo + (j0 ^ lo)];
-    x1[j0] = s1[64 * hi + 8 * lo + (j0 ^ lo)];
+  for (int j = 0; j < 8; ++j) {  // input j0 = j: value lo of thread (hi, j)
+    const int a = PHASE == 0 ? xslot(lo, j, hi) : xslot(j, hi, lo);
+    x0[j] = s0[a];
+    x1[j] = s1[a];
   }
   dft8<1>(x0);
   dft8<1>(x1);
 }
 
+// Inverse pair, PHASE 2: its first writes land in the slots the PHASE 1 forward read last.
 template <class Sync>
 TFB_HD void fft_inverse2(cd* x0, cd* x1, int t, const Twiddles* tw, cd* s0, cd* s1, Sync& sync) {
   const int hi = t >> 3, lo = t & 7;
   dft8<-1>(x0);
   dft8<-1>(x1);
-  sync();
-  s0[64 * hi + 8 * lo + lo] = x0[0];
-  s1[64 * hi + 8 * lo + lo] = x1[0];
   {
     const cd v = tw->tw2[1][lo];
     cd w = v;
+    const int a0 = xslot(0, hi, lo);
+    s0[a0] = x0[0];
+    s1[a0] = x1[0];
 #pragma unroll
-    for (int j0 = 1; j0 < 8; ++j0) {
-      s0[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x0[j0], w);
-      s1[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x1[j0], w);
+    for (int j0 = 1; j0 < 8; ++j0) {  // value j0 of thread (k0, k1) = (hi, lo)
+      const int a = xslot(j0, hi, lo);
+      s0[a] = cmulc(x0[j0], w);
+      s1[a] = cmulc(x1[j0], w);
       if (j0 < 7) w = cmul(w, v);
     }
   }
   sync();
 #pragma unroll
-  for (int k1 = 0; k1 < 8; ++k1) {
-    x0[k1] = s0[64 * hi + 8 * k1 + (lo ^ k1)];
-    x1[k1] = s1[64 * hi + 8 * k1 + (lo ^ k1)];
+  for (int k1 = 0; k1 < 8; ++k1) {  // thread (k0, j0) = (hi, lo): value j0 = lo of thread (hi, k1)
+    const int a = xslot(lo, hi, k1);
+    x0[k1] = s0[a];
+    x1[k1] = s1[a];
   }
   dft8<-1>(x0);
   dft8<-1>(x1);
-  sync();
 #pragma unroll
   for (int j1 = 0; j1 < 8; ++j1) {
-    s0[64 * hi + 8 * j1 + lo] = x0[j1];
-    s1[64 * hi + 8 * j1 + lo] = x1[j1];
+    const int a = xslot(lo, hi, j1);
+    s0[a] = x0[j1];
+    s1[a] = x1[j1];
   }
   sync();
   {
     cd w = tw->tw1[0][t];
     const cd g = tw->g[t];
 #pragma unroll
-    for (int k0 = 0; k0 < 8; ++k0) {
-      x0[k0] = cmulc(s0[64 * k0 + t], w);
-      x1[k0] = cmulc(s1[64 * k0 + t], w);
+    for (int k0 = 0; k0 < 8; ++k0) {  // thread (j1, j0) = (hi, lo): value j1 = hi of thread (k0, lo)
+      const int a = xslot(lo, k0, hi);
+      x0[k0] = cmulc(s0[a], w);
+      x1[k0] = cmulc(s1[a], w);
       if (k0 < 7) w = cmul(w, g);
     }
   }
@@ -377,7 +396,7 @@ TFB_HD void cmux_half(cd* out0, cd* out1, const uint32_t* acc, int abar, int i, 
     x0[m] = cd{digit_to_double(digit_field(vr, 0)), digit_to_double(digit_field(vi, 0))};
     x1[m] = cd{digit_to_double(digit_field(vr, 1)), digit_to_double(digit_field(vi, 1))};
   }
-  fft_forward2(x0, x1, t, tw, s0, s1, sync);
+  fft_forward2<P>(x0, x1, t, tw, s0, s1, sync);
   const cd* stage = bk.acquire(i, P);
 #pragma unroll
   for (int k2 = 0; k2 < 8; ++k2) {
