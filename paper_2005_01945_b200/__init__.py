@@ -54,6 +54,25 @@ from .linalg import (
     vec_add,
     vec_mul,
 )
+from .serialize import (
+    FormatError,
+    dump_eval_keys,
+    dump_int,
+    dump_key,
+    dump_matrix,
+    dump_params,
+    dump_sample,
+    dump_vector,
+    load_eval_keys,
+    load_int,
+    load_key,
+    load_key_file,
+    load_matrix,
+    load_params,
+    load_sample,
+    load_vector,
+    save_key,
+)
 from .scheduler import DEFAULT_MAX_BATCH, PARALLEL_BLOCK, JobBatch, PoolConfig, WorkerPool
 from .torus import (
     DEFAULT_ALPHA,

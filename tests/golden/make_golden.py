@@ -99,6 +99,36 @@ meta["circuits"] = counts
 meta["margins"] = {k.value: ref.gate_margin(k) for k in TWO_INPUT_KINDS}
 meta["fresh_bound"] = params.fresh_noise_bound
 
+# wire formats (encirc/serialize.py): bytes produced by the reference
+from encirc.linalg import encrypt_vector  # noqa: E402
+from encirc.serialize import dump_int, dump_key, dump_matrix, dump_params, dump_sample, dump_vector  # noqa: E402
+
+ser_eng = OracleBootstrapEngine(key, seed=9)
+ser_int = encrypt_int(ser_eng, 11, 4)
+ser_vec = encrypt_vector(ser_eng, [3, 5], 3)
+ser_mat = encrypt_matrix(ser_eng, [[1, 2], [3, 0]], 2)
+for name, blob in (("ser_params", dump_params(params)), ("ser_key11", dump_key(key)),
+                   ("ser_sample", dump_sample(fresh[0].sample)), ("ser_int", dump_int(ser_int)),
+                   ("ser_vector", dump_vector(ser_vec)), ("ser_matrix", dump_matrix(ser_mat))):
+    out[name] = np.frombuffer(blob, dtype=np.uint8)
+
+# rows of the reference's own harness on its cleartext engine, timing omitted (encirc/bench.py)
+from encirc import bench as ref_bench  # noqa: E402
+
+def harness_engine():
+    return ReferenceEngine(params, pool=WorkerPool(PoolConfig(workers=1)), seed=3)
+
+rows = []
+rows += ref_bench.bench_gate(harness_engine(), (4, 8, 16, 32), (GateKind.AND, GateKind.XOR))
+rows += ref_bench.bench_compound(harness_engine(), (1, 4, 8))
+rows += ref_bench.bench_add(harness_engine(), (16, 32), "bitwise", (1, 4))
+rows += ref_bench.bench_add(harness_engine(), (16,), "numberwise", (1,))
+rows += ref_bench.bench_mul(harness_engine(), (16,), "naive", (1, 4))
+rows += ref_bench.bench_mul(harness_engine(), (16,), "karatsuba", (1,))
+rows += ref_bench.bench_matmul(harness_engine(), (2, 4), "cannon")
+rows += ref_bench.bench_matmul(harness_engine(), (2,), "flat")
+meta["harness_rows"] = [r.record(omit_timing=True) for r in rows]
+
 np.savez_compressed(os.path.join(HERE, "reference_vectors.npz"), **out)
 with open(os.path.join(HERE, "reference_meta.json"), "w") as f:
     json.dump(meta, f, indent=1, sort_keys=True)

@@ -175,3 +175,41 @@ def test_noise_hygiene_over_many_gate_outputs(b200):
         rows, own = out, own2
         seen += len(out)
     assert seen == 10000
+
+
+def test_wire_formats_on_device_ciphertexts(key, eval_keys, golden):
+    """Engine seed 9: device-resident integers serialise to the reference's bytes and load back."""
+    from paper_2005_01945_b200 import B200Engine, dump_int, dump_matrix, dump_vector, load_int, load_matrix, load_vector
+
+    eng = B200Engine(key, seed=9, eval_keys=eval_keys)
+    x = encrypt_int(eng, 11, 4)
+    vec = encrypt_vector(eng, [3, 5], 3)
+    mat = encrypt_matrix(eng, [[1, 2], [3, 0]], 2)
+    assert dump_int(x) == golden["ser_int"].tobytes()
+    assert dump_vector(vec) == golden["ser_vector"].tobytes()
+    assert dump_matrix(mat) == golden["ser_matrix"].tobytes()
+    y = load_int(golden["ser_int"].tobytes(), eng)
+    assert decrypt_int(eng, add_bitwise(x, y)) == (11 + 11) % 16
+    assert decrypt_vector(eng, load_vector(dump_vector(vec_add(vec, vec)), eng)) == [6, 2]
+    assert decrypt_matrix(eng, load_matrix(golden["ser_matrix"].tobytes(), eng)) == [[1, 2], [3, 0]]
+
+
+def test_cli_runs_the_reference_experiments_on_the_gpu(tmp_path, golden):
+    import json
+
+    from paper_2005_01945_b200.cli import main
+
+    out = tmp_path / "rows.json"
+    assert main(["add", "--engine", "b200-tfhe", "--n", "16", "--ell", "1,4", "--seed", "3", "--workers", "1",
+                 "--format", "json", "--omit-timing", "--out", str(out)]) == 0
+    rows = [json.loads(line) for line in out.read_text().splitlines()]
+    want = [r for r in golden["meta"]["harness_rows"] if r["experiment"] in ("add-bitwise", "vec-add") and r["n"] == 16]
+    assert len(rows) == len(want) == 2
+    for got, ref in zip(rows, want):
+        assert got["engine"] == "b200-tfhe" and got["correct"] is True
+        for field in ("experiment", "n", "ell_or_rank", "workers", "single_gates", "compound_gates", "bootstraps",
+                      "batch_launches"):
+            assert got[field] == ref[field]
+    assert main(["gate", "--engine", "b200-tfhe", "--sizes", "4,300", "--max-size", "512", "--kinds", "nand,xor",
+                 "--seed", "3", "--out", str(tmp_path / "g.csv")]) == 0
+    assert main(["compound", "--engine", "b200-tfhe", "--sizes", "1,8", "--seed", "3", "--out", str(tmp_path / "c.csv")]) == 0
