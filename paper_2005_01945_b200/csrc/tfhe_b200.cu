@@ -30,6 +30,9 @@ static_assert(TFB_EXT_STRIDE == EXT_STRIDE, "header / device stride mismatch");
 // ------------------------------------------------------------------------------------
 // context
 // ------------------------------------------------------------------------------------
+constexpr int64_t HOST_CHUNK = 16384;  // gates per pipeline chunk of tfb_gate_launch_host
+constexpr int HOST_EVENTS = 8;         // event slots; a slot is reused 8 chunks later (long after it fired)
+
 struct tfb_ctx {
   int device = 0;
   tfb_params p{};
@@ -44,6 +47,8 @@ struct tfb_ctx {
   uint8_t* d_hkinds = nullptr;
   int32_t* d_hrows = nullptr;  // identity row indices
   int64_t host_cap = 0;
+  cudaStream_t s_in = nullptr, s_run = nullptr, s_out = nullptr;  // host-buffer launch pipeline
+  cudaEvent_t ev_in[HOST_EVENTS] = {}, ev_run[HOST_EVENTS] = {};
   int64_t launches = 0;
   int sm_count = 148;
   int force_kernel = 0;        // 0 auto, 1 = K1a (one ciphertext per CTA), 2 = K1b (ring), 3 = K1c (wide)
@@ -551,6 +556,13 @@ void tfb_ctx_destroy(tfb_ctx* ctx) {
   cudaFree(ctx->d_hx);
   cudaFree(ctx->d_hkinds);
   cudaFree(ctx->d_hrows);
+  if (ctx->s_in) {
+    cudaStreamDestroy(ctx->s_in);
+    cudaStreamDestroy(ctx->s_run);
+    cudaStreamDestroy(ctx->s_out);
+    for (auto e : ctx->ev_in) cudaEventDestroy(e);
+    for (auto e : ctx->ev_run) cudaEventDestroy(e);
+  }
   delete ctx;
 }
 
@@ -693,6 +705,7 @@ int tfb_gate_launch_host(tfb_ctx* ctx, const uint32_t* x, const uint32_t* y, con
     k_identity_rows<<<(unsigned)((3 * cap + 255) / 256), 256>>>(ctx->d_hrows, 3 * cap, 0);
     ctx->launches += 1;
     TFB_CUDA(ctx, cudaGetLastError());
+    TFB_CUDA(ctx, cudaStreamSynchronize(0));  // the pipeline streams below do not wait on the default stream
     ctx->host_cap = cap;
   }
   const int64_t cap = ctx->host_cap;
@@ -700,18 +713,41 @@ int tfb_gate_launch_host(tfb_ctx* ctx, const uint32_t* x, const uint32_t* y, con
   uint32_t* dx = ctx->d_hx;
   uint32_t* dy = ctx->d_hx + (size_t)cap * ROW_STRIDE;
   uint32_t* dout = ctx->d_hx + (size_t)2 * cap * ROW_STRIDE;
-  cudaStream_t st = 0;
-  TFB_CUDA(ctx, cudaMemcpy2DAsync(dx, dpitch, x, wpitch, wpitch, (size_t)k, cudaMemcpyHostToDevice, st));
-  TFB_CUDA(ctx, cudaMemcpy2DAsync(dy, dpitch, y, wpitch, wpitch, (size_t)k, cudaMemcpyHostToDevice, st));
-  TFB_CUDA(ctx, cudaMemcpyAsync(ctx->d_hkinds, kinds, (size_t)k, cudaMemcpyHostToDevice, st));
   if ((rc = ensure_ext(ctx, k))) return rc;
-  // rows: x = [0,cap), y = [cap, 2cap), out = [2cap, 3cap) of the d_hx pool
-  if ((rc = launch_blind_rotate(ctx, ctx->d_hx, ctx->d_hkinds, ctx->d_hrows, ctx->d_hrows + cap, ctx->d_ext, k,
-                                st)))
-    return rc;
-  if ((rc = launch_key_switch(ctx, ctx->d_ext, ctx->d_hx, ctx->d_hrows + 2 * cap, k, st))) return rc;
-  TFB_CUDA(ctx, cudaMemcpy2DAsync(out, wpitch, dout, dpitch, wpitch, (size_t)k, cudaMemcpyDeviceToHost, st));
-  TFB_CUDA(ctx, cudaStreamSynchronize(st));
+  if (!ctx->s_in) {
+    TFB_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
+    TFB_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->s_run, cudaStreamNonBlocking));
+    TFB_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev_in) TFB_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ctx->ev_run) TFB_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // Three-stage pipeline over chunks of the launch: host->device copy of chunk c+1 and
+  // device->host copy of chunk c-1 overlap the kernels of chunk c (rows: x = [0,cap),
+  // y = [cap,2cap), out = [2cap,3cap) of the d_hx pool; chunks use disjoint row ranges).
+  const int64_t chunk = k >= 4 * HOST_CHUNK ? HOST_CHUNK : k;
+  int slot = 0;
+  for (int64_t c0 = 0; c0 < k; c0 += chunk, slot = (slot + 1) % HOST_EVENTS) {
+    const int64_t kc = (k - c0 < chunk) ? k - c0 : chunk;
+    const size_t doff = (size_t)c0 * ROW_STRIDE, hoff = (size_t)c0 * (ctx->p.n + 1);
+    TFB_CUDA(ctx, cudaMemcpy2DAsync(dx + doff, dpitch, x + hoff, wpitch, wpitch, (size_t)kc, cudaMemcpyHostToDevice,
+                                    ctx->s_in));
+    TFB_CUDA(ctx, cudaMemcpy2DAsync(dy + doff, dpitch, y + hoff, wpitch, wpitch, (size_t)kc, cudaMemcpyHostToDevice,
+                                    ctx->s_in));
+    TFB_CUDA(ctx, cudaMemcpyAsync(ctx->d_hkinds + c0, kinds + c0, (size_t)kc, cudaMemcpyHostToDevice, ctx->s_in));
+    TFB_CUDA(ctx, cudaEventRecord(ctx->ev_in[slot], ctx->s_in));
+    TFB_CUDA(ctx, cudaStreamWaitEvent(ctx->s_run, ctx->ev_in[slot], 0));
+    uint32_t* ext = ctx->d_ext + (size_t)c0 * EXT_STRIDE;
+    if ((rc = launch_blind_rotate(ctx, ctx->d_hx, ctx->d_hkinds + c0, ctx->d_hrows + c0, ctx->d_hrows + cap + c0, ext,
+                                  kc, ctx->s_run)))
+      return rc;
+    if ((rc = launch_key_switch(ctx, ext, ctx->d_hx, ctx->d_hrows + 2 * cap + c0, kc, ctx->s_run))) return rc;
+    TFB_CUDA(ctx, cudaEventRecord(ctx->ev_run[slot], ctx->s_run));
+    TFB_CUDA(ctx, cudaStreamWaitEvent(ctx->s_out, ctx->ev_run[slot], 0));
+    TFB_CUDA(ctx, cudaMemcpy2DAsync(out + hoff, wpitch, dout + doff, dpitch, wpitch, (size_t)kc,
+                                    cudaMemcpyDeviceToHost, ctx->s_out));
+  }
+  TFB_CUDA(ctx, cudaStreamSynchronize(ctx->s_out));
+  TFB_CUDA(ctx, cudaStreamSynchronize(ctx->s_run));
   return TFB_OK;
 }
 
