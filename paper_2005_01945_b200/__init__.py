@@ -9,6 +9,17 @@ include/tfhe_b200.h).  Importing this package does not need a GPU;
 constructing a `B200Engine` does, and there is no CPU fallback.
 """
 
+from .datasets import (
+    KIND_BINARY,
+    KIND_NUMERICAL,
+    KINDS,
+    Dataset,
+    DatasetFormatError,
+    read_csv,
+    synthesize,
+    to_csv_text,
+    write_csv,
+)
 from .engine import (
     TWO_INPUT_KINDS,
     B200Engine,
@@ -72,6 +83,14 @@ from .serialize import (
     load_sample,
     load_vector,
     save_key,
+)
+from .regression import (
+    DEFAULT_BITS,
+    RegressionReport,
+    SingularSystemError,
+    VerificationError,
+    fit_encrypted,
+    solve_exact,
 )
 from .scheduler import DEFAULT_MAX_BATCH, PARALLEL_BLOCK, JobBatch, PoolConfig, WorkerPool
 from .torus import (

@@ -129,6 +129,19 @@ rows += ref_bench.bench_matmul(harness_engine(), (2, 4), "cannon")
 rows += ref_bench.bench_matmul(harness_engine(), (2,), "flat")
 meta["harness_rows"] = [r.record(omit_timing=True) for r in rows]
 
+# encrypted linear regression (encirc/regression.py, encirc/datasets.py) on the cleartext engine
+from encirc import fit_encrypted, synthesize, to_csv_text  # noqa: E402
+
+reg = {}
+for kind in ("numerical", "binary"):
+    ds = synthesize(kind, 12, 3, seed=4)
+    eng_r = ReferenceEngine(params, pool=WorkerPool(PoolConfig(workers=1, max_batch=1 << 22)))
+    rep = fit_encrypted(eng_r, ds, bits=12)
+    reg[kind] = {"csv": to_csv_text(ds), "truth": list(ds.coefficients),
+                 "coefficients": [[c.numerator, c.denominator] for c in rep.coefficients],
+                 "gram": [list(r) for r in rep.gram], "moment": list(rep.moment), "stats": eng_r.stats.as_record()}
+meta["regression"] = reg
+
 np.savez_compressed(os.path.join(HERE, "reference_vectors.npz"), **out)
 with open(os.path.join(HERE, "reference_meta.json"), "w") as f:
     json.dump(meta, f, indent=1, sort_keys=True)

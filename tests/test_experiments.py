@@ -64,4 +64,12 @@ def test_cli_exit_codes_and_reproducible_rows(tmp_path, capsys):
     key = tmp_path / "k.bin"
     assert main(["keygen", "--out", str(key), "--seed", "4"]) == 0
     assert main(["gate", "--engine", "b200-tfhe", "--key", str(tmp_path / "missing.bin")]) == 2
+    data = tmp_path / "d.csv"
+    assert main(["dataset", "--rows", "8", "--attrs", "2", "--kind", "binary", "--seed", "2", "--out", str(data)]) == 0
+    assert main(["linreg", str(data), "--engine", "reference", "--bits", "8", "--format", "json",
+                 "--out", str(tmp_path / "l.json")]) == 0
+    assert json.loads((tmp_path / "l.json").read_text())["experiment"] == "linreg-binary"
+    singular = tmp_path / "s.csv"
+    singular.write_text("a,b,y\n1,1,2\n1,1,2\n")
+    assert main(["linreg", str(singular), "--engine", "reference", "--bits", "8"]) == 2
     capsys.readouterr()

@@ -213,3 +213,12 @@ def test_cli_runs_the_reference_experiments_on_the_gpu(tmp_path, golden):
     assert main(["gate", "--engine", "b200-tfhe", "--sizes", "4,300", "--max-size", "512", "--kinds", "nand,xor",
                  "--seed", "3", "--out", str(tmp_path / "g.csv")]) == 0
     assert main(["compound", "--engine", "b200-tfhe", "--sizes", "1,8", "--seed", "3", "--out", str(tmp_path / "c.csv")]) == 0
+
+
+def test_encrypted_regression_on_the_gpu(key, eval_keys, golden):
+    from paper_2005_01945_b200 import B200Engine
+    from tests.test_regression import check_regression_against_reference
+
+    check_regression_against_reference(
+        lambda: B200Engine(key, seed=3, pool=WorkerPool(PoolConfig(workers=1, max_batch=1 << 22)), eval_keys=eval_keys),
+        golden)
