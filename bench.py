@@ -390,8 +390,18 @@ def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_b200(args)
+        return
+    if args.gpus > 1 and "RANK" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: start one rank per GPU ourselves
+        import socket
+
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
+    run_b200(args)
 
 
 if __name__ == "__main__":

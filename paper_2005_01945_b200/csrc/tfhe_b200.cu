@@ -147,8 +147,9 @@ __global__ void __launch_bounds__(FFT_THREADS, TFB_K1_MIN_BLOCKS) k_gate_bootstr
   const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
   BlockSync sync;
   LdgBk bk{bkf};
+  NoPark park;
   gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, ext + g * EXT_STRIDE,
-                 (int)threadIdx.x, sync);
+                 (int)threadIdx.x, sync, park);
 }
 
 // ------------------------------------------------------------------------------------
@@ -205,39 +206,97 @@ __global__ void __launch_bounds__(K1C_THREADS, 1) k_gate_bootstrap_wide(
 constexpr int K1B_GROUPS = TFB_K1B_GROUPS;
 constexpr int K1B_THREADS = K1B_GROUPS * FFT_THREADS;
 constexpr int STAGE_BYTES = STAGE_CD * (int)sizeof(cd);
-// dynamic smem: twiddles | ring[2][STAGE_CD] | mbarriers (64 B) | groups
-constexpr int K1B_HEADER = (int)sizeof(Twiddles) + 2 * STAGE_BYTES + 64;
+#ifndef TFB_K1B_SLOTS
+#define TFB_K1B_SLOTS 2  // measured: 3 slots (groups free to drift a whole CMux apart) is 3.7% slower than 2
+#endif
+constexpr int K1B_SLOTS = TFB_K1B_SLOTS;
+// dynamic smem: twiddles | ring[K1B_SLOTS][STAGE_CD] | mbarriers (64 B) | groups
+constexpr int K1B_HEADER = (int)sizeof(Twiddles) + K1B_SLOTS * STAGE_BYTES + 64;
+
+// ---- tensor-memory parking of the CMux accumulators ------------------------------------
+// TMEM (256 KB per SM) is reachable only through tcgen05.ld/st; with the 32x32b shape thread
+// i of a warp owns lane 32*(warp%4)+i and any columns, i.e. it is private per-thread storage
+// the size of the register file.  Between the two halves of a CMux the 16 complex
+// accumulators of a thread (64 words) are parked there, which removes them from the
+// register budget of the second paired transform.
+#ifndef TFB_K1B_TMEM
+#define TFB_K1B_TMEM 0  // measured: 6 groups x 168 regs with parked accumulators = 4 groups x 255 regs without (93.9 vs 93.6 ms per 16 Ki gates)
+#endif
+struct TmemPark {
+  static constexpr bool parks = true;
+  uint32_t taddr;  // (lane << 16) | first column of this warp's 64-column slice
+  __device__ __forceinline__ void store(const cd* o0, const cd* o1) {
+    uint32_t r[64];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      r[8 * k + 0] = (uint32_t)__double2loint(o0[k].re);
+      r[8 * k + 1] = (uint32_t)__double2hiint(o0[k].re);
+      r[8 * k + 2] = (uint32_t)__double2loint(o0[k].im);
+      r[8 * k + 3] = (uint32_t)__double2hiint(o0[k].im);
+      r[8 * k + 4] = (uint32_t)__double2loint(o1[k].re);
+      r[8 * k + 5] = (uint32_t)__double2hiint(o1[k].re);
+      r[8 * k + 6] = (uint32_t)__double2loint(o1[k].im);
+      r[8 * k + 7] = (uint32_t)__double2hiint(o1[k].im);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)  // four 16-column stores
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+          "%14, %15, %16};" ::"r"(taddr + 16 * q),
+          "r"(r[16 * q + 0]), "r"(r[16 * q + 1]), "r"(r[16 * q + 2]), "r"(r[16 * q + 3]), "r"(r[16 * q + 4]),
+          "r"(r[16 * q + 5]), "r"(r[16 * q + 6]), "r"(r[16 * q + 7]), "r"(r[16 * q + 8]), "r"(r[16 * q + 9]),
+          "r"(r[16 * q + 10]), "r"(r[16 * q + 11]), "r"(r[16 * q + 12]), "r"(r[16 * q + 13]), "r"(r[16 * q + 14]),
+          "r"(r[16 * q + 15])
+          : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  __device__ __forceinline__ void load(int k2, cd& o0, cd& o1) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr + 8 * k2)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    o0 = cd{__hiloint2double((int)r[1], (int)r[0]), __hiloint2double((int)r[3], (int)r[2])};
+    o1 = cd{__hiloint2double((int)r[5], (int)r[4]), __hiloint2double((int)r[7], (int)r[6])};
+  }
+};
 
 struct RingBk {
   const cd* bkf;       // full spectral key in global memory
-  cd* ring;            // 2 stages in shared memory
-  uint64_t* full;      // [2] completes when a stage's bytes have landed
-  uint64_t* empty;     // [2] completes when every warp of the CTA released the stage
+  cd* ring;            // K1B_SLOTS stages in shared memory
+  uint64_t* full;      // [slots] completes when a stage's bytes have landed
+  uint64_t* empty;     // [slots] completes when every warp of the CTA released the stage
   int stage;           // next stage this thread will consume (2*i + p)
   int n_stages;
   bool producer;       // exactly one thread of the CTA issues the copies
 
+  static __device__ __forceinline__ int slot(int s) { return s % K1B_SLOTS; }
+  static __device__ __forceinline__ uint32_t parity(int s) { return (uint32_t)(s / K1B_SLOTS) & 1u; }
   __device__ __forceinline__ void issue(int s) {
-    mbar_expect_tx(&full[s & 1], STAGE_BYTES);
-    bulk_load(ring + (size_t)(s & 1) * STAGE_CD, bkf + (size_t)s * STAGE_CD, STAGE_BYTES, &full[s & 1]);
+    mbar_expect_tx(&full[slot(s)], STAGE_BYTES);
+    bulk_load(ring + (size_t)slot(s) * STAGE_CD, bkf + (size_t)s * STAGE_CD, STAGE_BYTES, &full[slot(s)]);
   }
-  // refill the slot stage-1 used with stage+1, once every warp has released it
+  // On entering stage s the producer requests stage s+1.  It lands in the slot stage
+  // s+1-K1B_SLOTS used, which every warp must have released: with 2 slots that is stage s-1
+  // (the producer's group trails the slowest group), with 3 slots stage s-2 (groups may
+  // drift a whole CMux apart before anyone waits).
   __device__ __forceinline__ void produce_ahead() {
-    if (producer && stage >= 1 && stage + 1 < n_stages) {
-      const int prev = stage - 1;
-      mbar_wait(&empty[prev & 1], (uint32_t)(prev >> 1) & 1u);
-      issue(stage + 1);
+    const int next = stage + 1;
+    if (producer && stage >= 1 && next < n_stages) {
+      if (next >= K1B_SLOTS) mbar_wait(&empty[slot(next)], parity(next - K1B_SLOTS));
+      issue(next);
     }
   }
   __device__ __forceinline__ const cd* acquire(int, int) {
     produce_ahead();
-    mbar_wait(&full[stage & 1], (uint32_t)(stage >> 1) & 1u);
-    return ring + (size_t)(stage & 1) * STAGE_CD;
+    mbar_wait(&full[slot(stage)], parity(stage));
+    return ring + (size_t)slot(stage) * STAGE_CD;
   }
   __device__ __forceinline__ cd load(const cd* q) const { return *q; }
   __device__ __forceinline__ void release() {
     __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[stage & 1]);
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot(stage)]);
     ++stage;
   }
   __device__ __forceinline__ void skip(int) {
@@ -256,7 +315,7 @@ __global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
   extern __shared__ __align__(128) unsigned char smem[];
   Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
   cd* ring = reinterpret_cast<cd*>(smem + sizeof(Twiddles));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sizeof(Twiddles) + 2 * STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sizeof(Twiddles) + K1B_SLOTS * STAGE_BYTES);
   const int grp = threadIdx.x / FFT_THREADS, t = threadIdx.x % FFT_THREADS;
   unsigned char* mine = smem + K1B_HEADER + (size_t)grp * group_smem(n);
   cd* s0 = reinterpret_cast<cd*>(mine);
@@ -266,12 +325,12 @@ __global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
 
   for (int i = threadIdx.x; i < (int)(sizeof(Twiddles) / sizeof(cd)); i += K1B_THREADS)
     reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
-  RingBk bk{bkf, ring, bars, bars + 2, 0, 2 * n, threadIdx.x == 0};
+  RingBk bk{bkf, ring, bars, bars + K1B_SLOTS, 0, 2 * n, threadIdx.x == 0};
   if (threadIdx.x == 0) {
-    mbar_init(&bk.full[0], 1);
-    mbar_init(&bk.full[1], 1);
-    mbar_init(&bk.empty[0], K1B_THREADS / 32);
-    mbar_init(&bk.empty[1], K1B_THREADS / 32);
+    for (int j = 0; j < K1B_SLOTS; ++j) {
+      mbar_init(&bk.full[j], 1);
+      mbar_init(&bk.empty[j], K1B_THREADS / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -287,7 +346,30 @@ __global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
   const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
   uint32_t* dst = want < k ? ext + g * EXT_STRIDE : reinterpret_cast<uint32_t*>(s0);  // scratch sink
   GroupSync sync{grp + 1};
-  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, dst, t, sync);
+#if TFB_K1B_TMEM
+  // 64 columns per warp; warps w, w+4, w+8, ... share a lane quarter and take consecutive slices
+  constexpr uint32_t kTmemCols = (K1B_THREADS / 128) * 64 <= 64 ? 64 : ((K1B_THREADS / 128) * 64 <= 128 ? 128 : 256);
+  __shared__ uint32_t tmem_base;
+  const uint32_t warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  TmemPark park{tmem_base + (((warp & 3u) * 32u) << 16) + (warp >> 2) * 64u};
+  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, dst, t, sync, park);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols) : "memory");
+#else
+  NoPark park;
+  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, dst, t, sync, park);
+#endif
 }
 
 // ------------------------------------------------------------------------------------

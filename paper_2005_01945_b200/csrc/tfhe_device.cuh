@@ -385,9 +385,18 @@ struct GlobalBk {  // plain pointer into the full key (host emulation, key setup
 // forward transform, MAC against stage (i, p).  P == 0 initialises the output
 // accumulators instead of adding to them, so they are not live (64 registers)
 // during the first paired transform.
-template <int P, class Sync, class BkSource>
+// A Park policy may hold the 16 accumulator values of a thread outside the register file
+// between the two halves of a CMux (the B200 kernel parks them in tensor memory):
+//   store(out0, out1) after the first half, load(k2, o0, o1) inside the second half's MAC.
+struct NoPark {
+  static constexpr bool parks = false;
+  TFB_HD void store(const cd*, const cd*) {}
+  TFB_HD void load(int, cd&, cd&) {}
+};
+
+template <int P, class Sync, class BkSource, class Park>
 TFB_HD void cmux_half(cd* out0, cd* out1, const uint32_t* acc, int abar, int i, BkSource& bk, int t,
-                      const Twiddles* tw, cd* s0, cd* s1, Sync& sync) {
+                      const Twiddles* tw, cd* s0, cd* s1, Sync& sync, Park& park) {
   cd x0[8], x1[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
@@ -404,6 +413,7 @@ TFB_HD void cmux_half(cd* out0, cd* out1, const uint32_t* acc, int abar, int i, 
       out0[k2] = cmul(x0[k2], bk.load(stage + stage_index(k2, 0, 0, t)));
       out1[k2] = cmul(x0[k2], bk.load(stage + stage_index(k2, 0, 1, t)));
     } else {
+      if (Park::parks) park.load(k2, out0[k2], out1[k2]);
       cmac(out0[k2], x0[k2], bk.load(stage + stage_index(k2, 0, 0, t)));
       cmac(out1[k2], x0[k2], bk.load(stage + stage_index(k2, 0, 1, t)));
     }
@@ -417,12 +427,13 @@ TFB_HD void cmux_half(cd* out0, cd* out1, const uint32_t* acc, int abar, int i, 
 // Every thread of the 64-thread group calls this; `sync` is the group barrier.
 // Both gadget levels of one accumulator polynomial are transformed as a pair,
 // then both output polynomials are inverse-transformed as a pair.
-template <class Sync, class BkSource>
+template <class Sync, class BkSource, class Park>
 TFB_HD void cmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, const Twiddles* tw, cd* s0, cd* s1,
-                      Sync& sync) {
+                      Sync& sync, Park& park) {
   cd out0[8], out1[8];
-  cmux_half<0>(out0, out1, acc, abar, i, bk, t, tw, s0, s1, sync);
-  cmux_half<1>(out0, out1, acc, abar, i, bk, t, tw, s0, s1, sync);
+  cmux_half<0>(out0, out1, acc, abar, i, bk, t, tw, s0, s1, sync, park);
+  if (Park::parks) park.store(out0, out1);
+  cmux_half<1>(out0, out1, acc, abar, i, bk, t, tw, s0, s1, sync, park);
   fft_inverse2(out0, out1, t, tw, s0, s1, sync);
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
@@ -484,10 +495,10 @@ TFB_HD void bootstrap_extract(const uint32_t* sm_acc, uint32_t* ext, int tid, in
 //   x_row, y_row: pool rows (n mask words then the body)
 //   sm_acc: 2N words, sm_abar: n+1 uint16, s0/s1: 512 cd each (exchange buffers)
 //   ext: N+1 words out (extracted LWE sample under the ring key)
-template <class Sync, class BkSource>
+template <class Sync, class BkSource, class Park>
 TFB_HD void gate_bootstrap(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu,
                            BkSource& bk, const Twiddles* tw, uint32_t* sm_acc, uint16_t* sm_abar,
-                           cd* s0, cd* s1, uint32_t* ext, int t, Sync& sync) {
+                           cd* s0, cd* s1, uint32_t* ext, int t, Sync& sync, Park& park) {
   bootstrap_prologue(x_row, y_row, kind, n, mu, sm_acc, sm_abar, t, FFT_THREADS, sync);
 #pragma unroll 1
   for (int i = 0; i < n; ++i) {
@@ -496,7 +507,7 @@ TFB_HD void gate_bootstrap(const uint32_t* x_row, const uint32_t* y_row, int kin
       bk.skip(i);
       continue;
     }
-    cmux_step(sm_acc, abar, i, bk, t, tw, s0, s1, sync);
+    cmux_step(sm_acc, abar, i, bk, t, tw, s0, s1, sync, park);
   }
   bootstrap_extract(sm_acc, ext, t, FFT_THREADS);
 }

@@ -122,8 +122,9 @@ void emu_gate_bootstrap(const uint32_t* x, const uint32_t* y, const uint8_t* kin
     std::vector<uint16_t> abar(n + 1);
     run_group([&](int t, BarrierSync& s) {
       GlobalBk bk{bkf};
+      NoPark park;
       gate_bootstrap(x + g * (n + 1), y + g * (n + 1), (int)kinds[g], n, mu, bk, &tw, acc.data(), abar.data(),
-                     bufA.data(), bufB.data(), ext.data(), t, s);
+                     bufA.data(), bufB.data(), ext.data(), t, s, park);
     });
     for (int j = 0; j <= RING_N; ++j) ext_out[g * (RING_N + 1) + j] = ext[j];
   }
