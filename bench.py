@@ -52,6 +52,7 @@ def parse_args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--batch", type=int, default=1 << 16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-circuits", action="store_true")
     return ap.parse_args()
 
 
@@ -372,9 +373,41 @@ def run_b200(args) -> None:
             "value": real_value, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": "256 NAND gates, oracle/tfhe_gate_oracle.c double-FFT path (real TFHE bootstrap + key switch); "
                       "NOT the reference -- the like-for-like CPU comparator", "correct": real_ok}
+    if world == 1 and not args.no_circuits:
+        line["circuits"] = time_circuits(local)
     print(json.dumps(line))
     if distributed:
         dist.destroy_process_group()
+
+
+def time_circuits(device: int) -> dict:
+    """The second half of BASELINE.json's metric: 32-bit encrypted add / multiply through the
+    public engine API (latency-bound: 96 and 961 dependent launches), results verified."""
+    from paper_2005_01945_b200 import (
+        B200Engine, LweParams, PoolConfig, WorkerPool, add_bitwise, decrypt_int, encrypt_int, keygen, mul_naive,
+    )
+
+    eng = B200Engine(keygen(LweParams(), seed=KEY_SEED), seed=ENGINE_SEED, device=device,
+                     pool=WorkerPool(PoolConfig(workers=1, max_batch=1 << 16)))
+    rng = np.random.default_rng((ENGINE_SEED, 2))
+    a, b = (int(v) for v in rng.integers(0, 1 << 32, size=2, dtype=np.uint64))
+    x, y = encrypt_int(eng, a, 32), encrypt_int(eng, b, 32)
+    out = {}
+    for name, fn, want in (("add32", add_bitwise, (a + b) % (1 << 32)), ("mul32", mul_naive, a * b)):
+        fn(encrypt_int(eng, 1, 32), encrypt_int(eng, 1, 32)) if name == "add32" else None  # warm the launch path
+        eng.synchronize()
+        eng.reset_stats()
+        t0 = time.perf_counter()
+        res = fn(x, y)
+        eng.synchronize()
+        dt = time.perf_counter() - t0
+        out[name] = {"seconds": dt, "ops_per_s": 1.0 / dt, "bootstraps": eng.stats.bootstraps,
+                     "launches": eng.stats.batch_launches, "correct": decrypt_int(eng, res) == want}
+    out["reference_cpu_seconds"] = {"add32": 0.018, "mul32": 0.281,
+                                    "source": "BASELINE.md section 3: the reference's oracle engine on the build "
+                                              "container (not a bootstrap)"}
+    out["paper_gtx1080_seconds"] = {"add32": 1.99, "mul32": 33.99, "source": "BASELINE.md section 2 (PAPER.md:802-810, 862-864)"}
+    return out
 
 
 def _measured_hbm():

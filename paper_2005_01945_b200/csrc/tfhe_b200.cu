@@ -1,10 +1,12 @@
 // libtfhe_b200.so -- sm_100a kernels and the C ABI declared in include/tfhe_b200.h.
 //
 // Kernels
-//   K1 k_gate_bootstrap   fused gate linear form + mod switch + n-step CMux blind
-//                         rotation + sample extract; one ciphertext per 64-thread
-//                         group, ACC resident in shared memory, FP64 negacyclic FFT
-//                         in registers (tfhe_device.cuh)
+//   K1 fused gate linear form + mod switch + n-step CMux blind rotation + sample extract;
+//      ACC resident in shared memory, FP64 negacyclic FFT in registers (tfhe_device.cuh):
+//      K1b k_gate_bootstrap_ring  4 gates per CTA, spectral key staged by TMA through an
+//                                 mbarrier ring (launches of >= 4 gates per SM)
+//      K1a k_gate_bootstrap       one gate per 64-thread CTA, key through L1/L2
+//      K1c k_gate_bootstrap_wide  one gate over four thread groups (latency path)
 //   K2 k_key_switch       batched N -> n key switch as an integer rank-8192 update,
 //                         32 ciphertexts x 512 columns per CTA, digits in smem
 //   K3 k_bk_transform     one-time: raw TRGSW rows -> spectral key in K1's register
@@ -37,7 +39,7 @@ struct tfb_ctx {
   int device = 0;
   tfb_params p{};
   bool keys_loaded = false;
-  cd* d_bkf = nullptr;         // [n][4][8][2][64] cd, prescaled by 1/512
+  cd* d_bkf = nullptr;         // staged layout [n][p][k2][lvl][c][t] (cd), prescaled by 1/512
   int32_t* d_ksk = nullptr;    // [N*t][ROW_STRIDE]
   Twiddles* d_tw = nullptr;
   uint32_t* d_ext = nullptr;   // scratch [cap][EXT_STRIDE]
@@ -127,7 +129,7 @@ __device__ __forceinline__ void bulk_load(void* dst_smem, const void* src_gmem, 
 constexpr int GROUP_SMEM_FIXED = 2 * HALF_N * (int)sizeof(cd) + 2 * RING_N * (int)sizeof(uint32_t);
 __host__ __device__ constexpr int group_smem(int n) { return GROUP_SMEM_FIXED + ((n + 1) * 2 + 15) / 16 * 16; }
 #ifndef TFB_K1_MIN_BLOCKS
-#define TFB_K1_MIN_BLOCKS 6
+#define TFB_K1_MIN_BLOCKS 4  // 255 registers, no spills: K1a serves launches of 2-4 gates per SM
 #endif
 
 __global__ void __launch_bounds__(FFT_THREADS, TFB_K1_MIN_BLOCKS) k_gate_bootstrap(
@@ -682,11 +684,9 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
 static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds, const int32_t* xr,
                                const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
   const int n = ctx->p.n;
-  // K1b keeps K1B_GROUPS ciphertexts on one SM; below one full wave of such CTAs the
-  // one-ciphertext-per-CTA kernel spreads the launch over more SMs and wins.
-  // K1c: up to two waves of one-gate-per-SM CTAs (4 groups per gate) beat six gates per SM on latency.
-  // K1b keeps K1B_GROUPS ciphertexts on one SM; below one full wave of such CTAs the
-  // one-ciphertext-per-CTA kernel K1a spreads the launch over more SMs and wins.
+  // K1c: up to two waves of one-gate-per-SM CTAs (four thread groups per gate) win on latency.
+  // K1b keeps K1B_GROUPS gates on one SM; below one full wave of such CTAs the
+  // one-gate-per-CTA kernel K1a spreads the launch over more SMs and wins.
   int which = ctx->force_kernel;
   if (!which) which = k <= 2 * ctx->sm_count ? 3 : (k >= (int64_t)ctx->sm_count * K1B_GROUPS ? 2 : 1);
   if (which == 3) {
