@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_bk_transform(const int32_t* __r
   for (int m = 0; m < 8; ++m)
     x[m] = cd{int32_to_double(src[t + 64 * m]), int32_to_double(src[t + 64 * m + HALF_N])};
   BlockSync sync;
-  fft_forward(x, t, tw, bufA, bufB, sync);
+  fft_forward(x, t, TableTw{tw, t}, bufA, bufB, sync);
   const double scale = 1.0 / HALF_N;
 #pragma unroll
   for (int k2 = 0; k2 < 8; ++k2)

@@ -163,18 +163,40 @@ TFB_HD cd fold_twist(int m) {
 // Spectral index held by (thread t, register k2) after a forward transform.
 TFB_HD int spectral_index(int t, int k2) { return (t >> 3) + 8 * (t & 7) + 64 * k2; }
 
+// Twiddle providers for the single transforms: the table in (shared or global) memory, or a
+// per-thread copy held in registers for the whole kernel (the latency kernel K1c has the
+// registers to spare and is limited by shared-memory traffic).
+struct TableTw {
+  const Twiddles* tw;
+  int t;
+  TFB_HD cd w1(int k) const { return tw->tw1[k][t]; }
+  TFB_HD cd w2(int k) const { return tw->tw2[k][t & 7]; }
+};
+struct RegTw {
+  cd a[8], b[8];
+  TFB_HD void load(const Twiddles* tw, int t) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      a[k] = tw->tw1[k][t];
+      b[k] = tw->tw2[k][t & 7];
+    }
+  }
+  TFB_HD cd w1(int k) const { return a[k]; }
+  TFB_HD cd w2(int k) const { return b[k]; }
+};
+
 // Forward negacyclic transform, unnormalised.
 //   in : x[m] = c_{t+64m} = a_{t+64m} + i a_{t+64m+512}   (untwisted)
 //   out: x[k2] = Z[spectral_index(t, k2)],
 //        Z_k = sum_j c_j exp(i pi j / N) exp(2 pi i j k / 512)
 // bufA/bufB: 512 cd each in shared memory.
-template <class Sync>
-TFB_HD void fft_forward(cd* x, int t, const Twiddles* tw, cd* bufA, cd* bufB, Sync& sync) {
+template <class Sync, class Tw>
+TFB_HD void fft_forward(cd* x, int t, const Tw& tw, cd* bufA, cd* bufB, Sync& sync) {
 #pragma unroll
   for (int m = 1; m < 8; ++m) x[m] = cmul(x[m], fold_twist(m));
   dft8<1>(x);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) bufA[64 * k + t] = cmul(x[k], tw->tw1[k][t]);
+  for (int k = 0; k < 8; ++k) bufA[64 * k + t] = cmul(x[k], tw.w1(k));
   sync();
   const int hi = t >> 3, lo = t & 7;
 #pragma unroll
@@ -182,7 +204,7 @@ TFB_HD void fft_forward(cd* x, int t, const Twiddles* tw, cd* bufA, cd* bufB, Sy
   dft8<1>(x);
   bufB[64 * hi + lo] = x[0];
 #pragma unroll
-  for (int k = 1; k < 8; ++k) bufB[64 * hi + 8 * k + (lo ^ k)] = cmul(x[k], tw->tw2[k][lo]);
+  for (int k = 1; k < 8; ++k) bufB[64 * hi + 8 * k + (lo ^ k)] = cmul(x[k], tw.w2(k));
   sync();
 #pragma unroll
   for (int j0 = 0; j0 < 8; ++j0) x[j0] = bufB[64 * hi + 8 * lo + (j0 ^ lo)];
@@ -192,13 +214,13 @@ TFB_HD void fft_forward(cd* x, int t, const Twiddles* tw, cd* bufA, cd* bufB, Sy
 // Inverse of fft_forward up to the factor 512 (folded into the key).
 //   in : x[k2] = S[spectral_index(t, k2)]
 //   out: x[m]  = c_{t+64m}  (re -> coefficient t+64m, im -> coefficient t+64m+512)
-template <class Sync>
-TFB_HD void fft_inverse(cd* x, int t, const Twiddles* tw, cd* bufA, cd* bufB, Sync& sync) {
+template <class Sync, class Tw>
+TFB_HD void fft_inverse(cd* x, int t, const Tw& tw, cd* bufA, cd* bufB, Sync& sync) {
   const int hi = t >> 3, lo = t & 7;
   dft8<-1>(x);
   bufA[64 * hi + 8 * lo + lo] = x[0];
 #pragma unroll
-  for (int j0 = 1; j0 < 8; ++j0) bufA[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x[j0], tw->tw2[j0][lo]);
+  for (int j0 = 1; j0 < 8; ++j0) bufA[64 * hi + 8 * lo + (j0 ^ lo)] = cmulc(x[j0], tw.w2(j0));
   sync();
 #pragma unroll
   for (int k1 = 0; k1 < 8; ++k1) x[k1] = bufA[64 * hi + 8 * k1 + (lo ^ k1)];
@@ -207,7 +229,7 @@ TFB_HD void fft_inverse(cd* x, int t, const Twiddles* tw, cd* bufA, cd* bufB, Sy
   for (int j1 = 0; j1 < 8; ++j1) bufB[64 * hi + 8 * j1 + lo] = x[j1];
   sync();
 #pragma unroll
-  for (int k0 = 0; k0 < 8; ++k0) x[k0] = cmulc(bufB[64 * k0 + t], tw->tw1[k0][t]);
+  for (int k0 = 0; k0 < 8; ++k0) x[k0] = cmulc(bufB[64 * k0 + t], tw.w1(k0));
   dft8<-1>(x);
 #pragma unroll
   for (int m = 1; m < 8; ++m) x[m] = cmulc(x[m], fold_twist(m));
@@ -530,6 +552,11 @@ TFB_HD void gate_bootstrap_wide(const uint32_t* x_row, const uint32_t* y_row, in
   cd* bufA = xbuf + (size_t)q * 2 * HALF_N;
   cd* bufB = bufA + HALF_N;
   bootstrap_prologue(x_row, y_row, kind, n, mu, sm_acc, sm_abar, tid, WIDE, csync);
+  RegTw rtw;
+  rtw.load(tw, t);
+  // Output polynomial c is inverse-transformed by group c.  A group keeps the product that
+  // stays with it in registers and publishes only what another group needs:
+  // red[q][c] is written for every (q, c) except (0, 0) and (1, 1).
 #pragma unroll 1
   for (int i = 0; i < n; ++i) {
     const int abar = sm_abar[i];
@@ -548,22 +575,25 @@ TFB_HD void gate_bootstrap_wide(const uint32_t* x_row, const uint32_t* y_row, in
       const uint32_t vi = rotated_diff(sm_acc + p * RING_N, t + 64 * m + HALF_N, abar) + DECOMP_OFFSET;
       x[m] = cd{digit_to_double(digit_field(vr, lvl)), digit_to_double(digit_field(vi, lvl))};
     }
-    fft_forward(x, t, tw, bufA, bufB, gsync);
+    fft_forward(x, t, rtw, bufA, bufB, gsync);
 #pragma unroll
     for (int k2 = 0; k2 < 8; ++k2) {
-      red[((q * 2 + 0) * 8 + k2) * FFT_THREADS + t] = cmul(x[k2], b0[k2]);
-      red[((q * 2 + 1) * 8 + k2) * FFT_THREADS + t] = cmul(x[k2], b1[k2]);
+      const cd p0 = cmul(x[k2], b0[k2]), p1 = cmul(x[k2], b1[k2]);
+      if (q != 0) red[((q * 2 + 0) * 8 + k2) * FFT_THREADS + t] = p0;
+      if (q != 1) red[((q * 2 + 1) * 8 + k2) * FFT_THREADS + t] = p1;
+      x[k2] = (q == 0) ? p0 : p1;  // meaningful for q < 2: the product this group keeps
     }
     csync();
     if (q < 2) {  // output polynomial c = q
 #pragma unroll
       for (int k2 = 0; k2 < 8; ++k2) {
-        cd s = red[((0 * 2 + q) * 8 + k2) * FFT_THREADS + t];
-        s = cadd(s, red[((1 * 2 + q) * 8 + k2) * FFT_THREADS + t]);
-        s = cadd(s, red[((2 * 2 + q) * 8 + k2) * FFT_THREADS + t]);
-        x[k2] = cadd(s, red[((3 * 2 + q) * 8 + k2) * FFT_THREADS + t]);
+        cd s = x[k2];
+#pragma unroll
+        for (int o = 0; o < 4; ++o)
+          if (o != q) s = cadd(s, red[((o * 2 + q) * 8 + k2) * FFT_THREADS + t]);
+        x[k2] = s;
       }
-      fft_inverse(x, t, tw, bufA, bufB, gsync);
+      fft_inverse(x, t, rtw, bufA, bufB, gsync);
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
         sm_acc[q * RING_N + t + 64 * m] += round_to_word(x[m].re);

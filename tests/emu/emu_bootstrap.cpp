@@ -66,7 +66,7 @@ void emu_bk_transform(const int32_t* bk_raw, int n, double* bkf_out) {
       cd x[8];
       for (int m = 0; m < 8; ++m)
         x[m] = cd{int32_to_double(src[t + 64 * m]), int32_to_double(src[t + 64 * m + HALF_N])};
-      fft_forward(x, t, &tw, bufA.data(), bufB.data(), s);
+      fft_forward(x, t, TableTw{&tw, t}, bufA.data(), bufB.data(), s);
       for (int k2 = 0; k2 < 8; ++k2)
         bkf[stage_offset((int)(ir / BK_ROWS), (int)(ir % BK_ROWS) / BK_L) + stage_index(k2, (int)(ir % BK_L), c, t)] =
             cd{x[k2].re / HALF_N, x[k2].im / HALF_N};
@@ -85,7 +85,7 @@ void emu_fft_forward(const int32_t* poly, double* spec_out) {
     cd x[8];
     for (int m = 0; m < 8; ++m)
       x[m] = cd{int32_to_double(src[t + 64 * m]), int32_to_double(src[t + 64 * m + HALF_N])};
-    fft_forward(x, t, &tw, bufA.data(), bufB.data(), s);
+    fft_forward(x, t, TableTw{&tw, t}, bufA.data(), bufB.data(), s);
     for (int k2 = 0; k2 < 8; ++k2) out[spectral_index(t, k2)] = x[k2];
   });
 }
@@ -102,7 +102,7 @@ void emu_fft_inverse(const double* spec_in, uint32_t* poly_out) {
       cd v = in[spectral_index(t, k2)];
       x[k2] = cd{v.re / HALF_N, v.im / HALF_N};
     }
-    fft_inverse(x, t, &tw, bufA.data(), bufB.data(), s);
+    fft_inverse(x, t, TableTw{&tw, t}, bufA.data(), bufB.data(), s);
     for (int m = 0; m < 8; ++m) {
       poly_out[t + 64 * m] = round_to_word(x[m].re);
       poly_out[t + 64 * m + HALF_N] = round_to_word(x[m].im);
