@@ -23,6 +23,7 @@
 
 #include "../../include/tfhe_b200.h"
 #include "tfhe_device.cuh"
+#include "tfhe_warp.cuh"
 
 using namespace tfb;
 
@@ -40,6 +41,8 @@ struct tfb_ctx {
   tfb_params p{};
   bool keys_loaded = false;
   cd* d_bkf = nullptr;         // staged layout [n][p][k2][lvl][c][t] (cd), prescaled by 1/512
+  cd* d_bkw = nullptr;         // K1d's staged layout [n][p][lvl][q][c][lane] (cd), prescaled by 1/512
+  WarpTwiddles* d_wtw = nullptr;
   int32_t* d_ksk = nullptr;    // [N*t][ROW_STRIDE]
   Twiddles* d_tw = nullptr;
   uint32_t* d_ext = nullptr;   // scratch [cap][EXT_STRIDE]
@@ -53,7 +56,7 @@ struct tfb_ctx {
   cudaEvent_t ev_in[HOST_EVENTS] = {}, ev_run[HOST_EVENTS] = {};
   int64_t launches = 0;
   int sm_count = 148;
-  int force_kernel = 0;        // 0 auto, 1 = K1a (one ciphertext per CTA), 2 = K1b (ring), 3 = K1c (wide)
+  int force_kernel = 0;        // 0 auto, 1 = K1a (one ciphertext per CTA), 2 = K1b (ring), 3 = K1c (wide), 4 = K1d (warp)
   std::string err;
 };
 
@@ -375,6 +378,221 @@ __global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
 }
 
 // ------------------------------------------------------------------------------------
+// K1d: fused gate bootstrap, ONE ciphertext per WARP, K1D_WARPS ciphertexts per CTA (one CTA
+//      per SM), arithmetic in tfhe_warp.cuh.  Radix-16 transforms: one shared-memory exchange
+//      and one shuffle stage per transform instead of two exchanges, no barrier other than
+//      __syncwarp inside the blind rotation; the spectral key comes through the same TMA ring
+//      as K1b (one 32 KB stage per (LWE index, accumulator polynomial), shared by all warps).
+// ------------------------------------------------------------------------------------
+#ifndef TFB_K1D_TMEM
+#define TFB_K1D_TMEM 1  // accumulators parked in tensor memory between the MAC stages
+#endif
+#ifndef TFB_K1D_WARPS
+#define TFB_K1D_WARPS 12  // 3 warps per scheduler: 168 registers each, accumulators parked in tensor memory
+#endif
+constexpr int K1D_WARPS = TFB_K1D_WARPS;
+constexpr int K1D_THREADS = K1D_WARPS * WARP_T;
+__host__ __device__ constexpr int warp_smem(int n) {
+  return WBUF_BYTES + 2 * RING_N * (int)sizeof(uint32_t) + ((n + 1) * 2 + 15) / 16 * 16;
+}
+constexpr int K1D_HEADER = (int)sizeof(WarpTwiddles) + K1B_SLOTS * STAGE_BYTES + 64;
+
+// Key ring of K1d.  Consumers wait on the full mbarrier of a slot; a slot is handed back by
+// counting releases, and the warp whose release is the last one issues the bulk copy of the
+// stage that reuses the slot (no dedicated producer: with a fixed producer thread every warp
+// of the CTA is gated by that thread's own progress, and the others spin on the barrier).
+struct WarpRing {
+  const cd* bkw;        // full spectral key in global memory
+  cd* ring;             // K1B_SLOTS stages in shared memory
+  uint64_t* full;       // [slots] completes when a stage's bytes have landed
+  uint32_t* released;   // [slots] warps that are done with the stage in the slot
+  int stage;            // next stage this warp will consume (2*i + p)
+  int n_stages;
+
+  static __device__ __forceinline__ int slot(int s) { return s % K1B_SLOTS; }
+  static __device__ __forceinline__ uint32_t parity(int s) { return (uint32_t)(s / K1B_SLOTS) & 1u; }
+  __device__ __forceinline__ void issue(int s) {
+    mbar_expect_tx(&full[slot(s)], STAGE_BYTES);
+    bulk_load(ring + (size_t)slot(s) * STAGE_CD, bkw + (size_t)s * STAGE_CD, STAGE_BYTES, &full[slot(s)]);
+  }
+  __device__ __forceinline__ const cd* acquire(int, int) {
+    mbar_wait(&full[slot(stage)], parity(stage));
+    return ring + (size_t)slot(stage) * STAGE_CD;
+  }
+  __device__ __forceinline__ cd load(const cd* q) const { return *q; }
+  __device__ __forceinline__ void release() {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      const int sl = slot(stage);
+      if (atomicAdd(&released[sl], 1u) == (uint32_t)(K1D_WARPS - 1)) {  // last one out refills the slot
+        released[sl] = 0;
+        __threadfence_block();
+        if (stage + K1B_SLOTS < n_stages) issue(stage + K1B_SLOTS);
+      }
+    }
+    ++stage;
+  }
+  __device__ __forceinline__ void skip(int) {
+    acquire(0, 0);
+    release();
+    acquire(0, 1);
+    release();
+  }
+};
+
+struct DevWarp {
+  __device__ __forceinline__ void operator()() const { __syncwarp(); }
+  __device__ __forceinline__ cd xchg16(cd v) const {
+    return cd{__shfl_xor_sync(0xffffffffu, v.re, 16), __shfl_xor_sync(0xffffffffu, v.im, 16)};
+  }
+};
+
+// Tensor-memory park of K1d: with the 32x32b shape lane i of warp w owns TMEM lane
+// 32*(w%4)+i and any columns, i.e. private per-lane storage with its own data path (measured:
+// 338 B/clk/SM loads, 895 B/clk/SM stores, concurrent with the shared-memory pipe;
+// tools/microbench/tmem_shfl_bw.cu).  A warp's slice is 128 columns: polynomial c at
+// columns 64c .. 64c+63, a chunk of PARK_CH complex values is 16 columns.
+struct TmemWPark {
+  uint32_t taddr;  // (lane << 16) | first column of this warp's slice
+  static __device__ __forceinline__ void unpack(const uint32_t* r, cd* o) {
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j)
+      o[j] = cd{__hiloint2double((int)r[4 * j + 1], (int)r[4 * j]), __hiloint2double((int)r[4 * j + 3], (int)r[4 * j + 2])};
+  }
+  static __device__ __forceinline__ void pack(const cd* o, uint32_t* r) {
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j) {
+      r[4 * j + 0] = (uint32_t)__double2loint(o[j].re);
+      r[4 * j + 1] = (uint32_t)__double2hiint(o[j].re);
+      r[4 * j + 2] = (uint32_t)__double2loint(o[j].im);
+      r[4 * j + 3] = (uint32_t)__double2hiint(o[j].im);
+    }
+  }
+  __device__ __forceinline__ void load_one(int c, int qb, cd* o) const {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n\ttcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr + 64 * c + 4 * qb)
+        : "memory");
+    unpack(r, o);
+  }
+  __device__ __forceinline__ void load(int qb, cd* o0, cd* o1) const {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%32];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+        "%30, %31}, [%33];\n\ttcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr + 4 * qb), "r"(taddr + 64 + 4 * qb)
+        : "memory");
+    unpack(r, o0);
+    unpack(r + 16, o1);
+  }
+  __device__ __forceinline__ void store_one(int c, int qb, const cd* o) const {
+    uint32_t r[16];
+    pack(o, r);
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr + 64 * c + 4 * qb),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+  }
+  __device__ __forceinline__ void store(int qb, const cd* o0, const cd* o1) const {
+    store_one(0, qb, o0);
+    store_one(1, qb, o1);
+  }
+  __device__ __forceinline__ void flush() const { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+  // level-1 digit words: columns 128 .. 143 of the slice (the MAC's flush() orders the store)
+  __device__ __forceinline__ void store_digits(const uint32_t* r) const {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr + 128),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+  }
+  __device__ __forceinline__ void load_digits(uint32_t* r) const {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n\ttcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr + 128)
+        : "memory");
+  }
+};
+constexpr uint32_t K1D_TMEM_SLICE = 144;  // columns per warp: 2 x 64 accumulators + 16 digit words
+
+__global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
+    const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
+    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
+    const cd* __restrict__ bkw, const WarpTwiddles* __restrict__ tw_global, uint32_t* __restrict__ ext,
+    int64_t k) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  WarpTwiddles* tw = reinterpret_cast<WarpTwiddles*>(smem);
+  cd* ring = reinterpret_cast<cd*>(smem + sizeof(WarpTwiddles));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sizeof(WarpTwiddles) + K1B_SLOTS * STAGE_BYTES);
+  const int wid = threadIdx.x / WARP_T, t = threadIdx.x % WARP_T;
+  unsigned char* mine = smem + K1D_HEADER + (size_t)wid * warp_smem(n);
+  void* buf = mine;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(mine + WBUF_BYTES);
+  uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
+
+  for (int i = threadIdx.x; i < (int)(sizeof(WarpTwiddles) / sizeof(cd)); i += K1D_THREADS)
+    reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
+  WarpRing bk{bkw, ring, bars, reinterpret_cast<uint32_t*>(bars + K1B_SLOTS), 0, 2 * n};
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < K1B_SLOTS; ++j) {
+      mbar_init(&bk.full[j], 1);
+      bk.released[j] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  // tensor memory: one slice per warp, warps w, w+4, w+8 share a lane quarter
+  constexpr uint32_t kTmemNeed = ((K1D_WARPS + 3) / 4) * K1D_TMEM_SLICE;
+  constexpr uint32_t kTmemCols = kTmemNeed <= 128 ? 128 : (kTmemNeed <= 256 ? 256 : 512);
+  static_assert(kTmemNeed <= 512, "tensor memory has 512 columns");
+  __shared__ uint32_t tmem_base;
+  if (wid == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (threadIdx.x == 0)
+    for (int j = 0; j < K1B_SLOTS; ++j) bk.issue(j);
+  // tail CTA: surplus warps redo the last ciphertext (keeps the ring protocol uniform) but do not store
+  const int64_t want = (int64_t)blockIdx.x * K1D_WARPS + wid;
+  const int64_t g = want < k ? want : k - 1;
+  const uint32_t* xr = pool + (int64_t)x_rows[g] * ROW_STRIDE;
+  const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
+  uint32_t* dst = want < k ? ext + g * EXT_STRIDE : nullptr;  // null: no extract
+  DevWarp w;
+#if TFB_K1D_TMEM
+  TmemWPark park{tmem_base + ((((uint32_t)wid & 3u) * 32u) << 16) + ((uint32_t)wid >> 2) * K1D_TMEM_SLICE};
+#else
+  RegPark park;
+#endif
+  gate_bootstrap_warp(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, buf, dst, t, w, park);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (wid == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols) : "memory");
+}
+
+// ------------------------------------------------------------------------------------
 // K2: key switch.  out[c][col] = (col == n ? ext_b[c] : 0) - sum_r digit[c][r] * ksk[r][col]
 //     r = i*KS_T + j over the N*KS_T digit rows; CTA tile = KS_CT ciphertexts x 512 columns.
 // ------------------------------------------------------------------------------------
@@ -482,6 +700,29 @@ __global__ void __launch_bounds__(FFT_THREADS) k_bk_transform(const int32_t* __r
         cd{x[k2].re * scale, x[k2].im * scale};
 }
 
+// same for K1d: one warp per raw polynomial -> bkw[i][p][lvl][q][c][lane]
+__global__ void __launch_bounds__(WARP_T) k_bk_transform_w(const int32_t* __restrict__ bk_raw,
+                                                           cd* __restrict__ bkw,
+                                                           const WarpTwiddles* __restrict__ tw) {
+  __shared__ __align__(16) unsigned char buf[WBUF_BYTES];
+  const int t = threadIdx.x;
+  const int64_t poly = blockIdx.x;
+  const int c = (int)(poly & 1);
+  const int64_t ir = poly >> 1;  // i*4 + r
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(bk_raw) + poly * RING_N;
+  cd x[WPTS];
+#pragma unroll
+  for (int m = 0; m < WPTS; ++m)
+    x[m] = cd{int32_to_double(src[t + 32 * m]), int32_to_double(src[t + 32 * m + HALF_N])};
+  DevWarp w;
+  wfft_forward(x, t, tw, buf, w);
+  const double scale = 1.0 / HALF_N;
+#pragma unroll
+  for (int q = 0; q < WPTS; ++q)
+    bkw[stage_offset((int)(ir / BK_ROWS), (int)(ir % BK_ROWS) / BK_L) + wstage_index((int)(ir % BK_L), q, c, t)] =
+        cd{x[q].re * scale, x[q].im * scale};
+}
+
 // ksk_raw[N*t][n+1] -> ksk[N*t][ROW_STRIDE], zero padded
 __global__ void k_ksk_layout(const int32_t* __restrict__ raw, int32_t* __restrict__ out, int n) {
   const int64_t r = blockIdx.x;
@@ -566,6 +807,8 @@ static void fill_twiddles(Twiddles* tw) {
   }
 }
 
+static void fill_warp_twiddles(WarpTwiddles* tw) { tfb::fill_warp_twiddles<long double>(tw, cosl, sinl); }
+
 static int ensure_ext(tfb_ctx* ctx, int64_t k) {
   if (k <= ctx->ext_cap) return TFB_OK;
   if (ctx->d_ext) TFB_CUDA(ctx, cudaFree(ctx->d_ext));
@@ -607,6 +850,15 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
   e = cudaMalloc(&ctx->d_tw, sizeof(Twiddles));
   if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw, h, sizeof(Twiddles), cudaMemcpyHostToDevice);
   delete h;
+  if (e == cudaSuccess) {
+    WarpTwiddles hw;
+    fill_warp_twiddles(&hw);
+    e = cudaMalloc(&ctx->d_wtw, sizeof(WarpTwiddles));
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_wtw, &hw, sizeof(WarpTwiddles), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gate_bootstrap_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             K1D_HEADER + K1D_WARPS * warp_smem(p->n));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gate_bootstrap, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(Twiddles) + group_smem(p->n));
@@ -634,6 +886,8 @@ void tfb_ctx_destroy(tfb_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaFree(ctx->d_bkf);
+  cudaFree(ctx->d_bkw);
+  cudaFree(ctx->d_wtw);
   cudaFree(ctx->d_ksk);
   cudaFree(ctx->d_tw);
   cudaFree(ctx->d_ext);
@@ -670,9 +924,11 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
   }
   if (!ctx->d_bkf) TFB_CUDA(ctx, cudaMalloc(&ctx->d_bkf, (size_t)n * BK_ROWS * 2 * HALF_N * sizeof(cd)));
   if (!ctx->d_ksk) TFB_CUDA(ctx, cudaMalloc(&ctx->d_ksk, (size_t)RING_N * KS_T * ROW_STRIDE * 4));
+  if (!ctx->d_bkw) TFB_CUDA(ctx, cudaMalloc(&ctx->d_bkw, (size_t)n * BK_ROWS * 2 * HALF_N * sizeof(cd)));
   k_bk_transform<<<n * BK_ROWS * 2, FFT_THREADS, 0, st>>>(d_bk, ctx->d_bkf, ctx->d_tw);
+  k_bk_transform_w<<<n * BK_ROWS * 2, WARP_T, 0, st>>>(d_bk, ctx->d_bkw, ctx->d_wtw);
   k_ksk_layout<<<RING_N * KS_T, 128, 0, st>>>(d_kr, ctx->d_ksk, n);
-  ctx->launches += 2;
+  ctx->launches += 3;
   TFB_CUDA(ctx, cudaGetLastError());
   TFB_CUDA(ctx, cudaStreamSynchronize(st));
   if (tmp_bk) cudaFree(tmp_bk);
@@ -689,7 +945,11 @@ static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* ki
   // one-gate-per-CTA kernel K1a spreads the launch over more SMs and wins.
   int which = ctx->force_kernel;
   if (!which) which = k <= 2 * ctx->sm_count ? 3 : (k >= (int64_t)ctx->sm_count * K1B_GROUPS ? 2 : 1);
-  if (which == 3) {
+  if (which == 4) {
+    const unsigned grid = (unsigned)((k + K1D_WARPS - 1) / K1D_WARPS);
+    k_gate_bootstrap_warp<<<grid, K1D_THREADS, K1D_HEADER + K1D_WARPS * warp_smem(n), st>>>(
+        (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ext, k);
+  } else if (which == 3) {
     k_gate_bootstrap_wide<<<(unsigned)k, K1C_THREADS, k1c_smem(n), st>>>(
         (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
   } else if (which == 2) {

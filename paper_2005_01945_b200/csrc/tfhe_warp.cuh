@@ -1,0 +1,424 @@
+// K1d building blocks: ONE ciphertext per WARP.
+//
+// The 64-thread kernels of tfhe_device.cuh move every transform through shared memory twice
+// (three radix-8 passes) and are bound by the shared-memory data pipe, not by FP64 (DESIGN.md
+// section 11).  Here a 32-lane warp owns a whole ciphertext and every lane carries 16 points:
+//   512 = 16 (registers) x 16 (registers, after ONE shared-memory exchange) x 2 (lane ^ 16, by
+//   warp shuffle), so a transform costs 128 + 32 instead of 256 shared-memory wavefronts per
+// ciphertext, there is no inter-warp barrier anywhere in the blind rotation (only __syncwarp),
+// and eight independent warps per SM hide each other's latencies.
+//
+// Same arithmetic contract as tfhe_device.cuh (exact integer result after rounding), same
+// `__host__ __device__` discipline: tests/emu drives this code with 32 host threads per warp.
+#pragma once
+#include "tfhe_device.cuh"
+
+#if defined(__CUDA_ARCH__)
+#define TFB_OPAQUE(v) asm volatile("" : "+r"(v))
+#else
+#define TFB_OPAQUE(v) (void)(v)
+#endif
+
+// The four forward and the two inverse transforms of a CMux as rolled loops (one copy of the
+// transform code: smaller instruction footprint, no scheduling across the stages) or unrolled.
+#ifndef TFB_K1D_ROLL
+#define TFB_K1D_ROLL 1
+#endif
+#if TFB_K1D_ROLL
+#define TFB_K1D_LOOP _Pragma("unroll 1")
+#else
+#define TFB_K1D_LOOP _Pragma("unroll")
+#endif
+
+namespace tfb {
+
+constexpr int WARP_T = 32;  // lanes per ciphertext
+constexpr int WPTS = 16;    // points per lane
+
+// Per-lane twiddles (t = lane, r = t & 15, h = t >> 4).  Lane h = 1 keeps its pass-1 outputs
+// rotated by 8 (register k holds frequency k ^ 8, see wfft_forward), so every lane runs two
+// chains of 8 pass-1 twiddles W512^{t k1} exp(i pi t / N) = exp(i pi t (1 + 4 k1) / 1024):
+//   sa[t] = the one of k1 = 8h       (registers 0..7,  then times g, g^2, ...)
+//   sb[t] = the one of k1 = 8(1-h)   (registers 8..15)
+//   g[t]  = exp(2 pi i t / 512)      ratio of consecutive twiddles
+//   c[t]  = (-1)^h exp(2 pi i r / 32)   twiddle of the odd half of the cross-lane radix-2 stage
+struct WarpTwiddles {
+  cd sa[WARP_T];
+  cd sb[WARP_T];
+  cd g[WARP_T];
+  cd c[WARP_T];
+};
+
+template <class Real>
+inline void fill_warp_twiddles(WarpTwiddles* tw, Real (*cosf_)(Real), Real (*sinf_)(Real)) {
+  const Real pi = (Real)3.141592653589793238462643383279502884L;
+  for (int t = 0; t < WARP_T; ++t) {
+    const int r = t & 15, h = t >> 4;
+    const Real aa = pi * (Real)(t * (1 + 32 * h)) / (Real)RING_N;
+    const Real ab = pi * (Real)(t * (1 + 32 * (1 - h))) / (Real)RING_N;
+    const Real ag = (Real)2 * pi * (Real)t / (Real)HALF_N;
+    const Real ac = (Real)2 * pi * (Real)r / (Real)32;
+    tw->sa[t] = cd{(double)cosf_(aa), (double)sinf_(aa)};
+    tw->sb[t] = cd{(double)cosf_(ab), (double)sinf_(ab)};
+    tw->g[t] = cd{(double)cosf_(ag), (double)sinf_(ag)};
+    tw->c[t] = cd{(double)(h ? -cosf_(ac) : cosf_(ac)), (double)(h ? -sinf_(ac) : sinf_(ac))};
+  }
+}
+
+// exp(i pi m / 32), m in [0, 16]: register part of the twist; exp(i pi j / 16) = twist16(2 j).
+// On the device the table sits in the constant bank, so that FP64 instructions take these
+// factors as c[][] operands: as literals the compiler hoists them out of the blind-rotation
+// loop into ~70 registers and then spills them.
+#define TFB_TWIST16_VALUES                                                                                   \
+  {1.0, 0.9951847266721969, 0.9807852804032304, 0.9569403357322088, 0.9238795325112867, 0.881921264348355,  \
+   0.8314696123025452, 0.773010453362737, 0.7071067811865476, 0.6343932841636455, 0.5555702330196023,       \
+   0.4713967368259978, 0.3826834323650898, 0.2902846772544623, 0.1950903220161283, 0.0980171403295608, 0.0}
+#if defined(__CUDACC__)
+__constant__ double kTwist16Dev[17] = TFB_TWIST16_VALUES;
+#endif
+TFB_HD cd twist16(int m) {
+#if defined(__CUDA_ARCH__)
+  return cd{kTwist16Dev[m], kTwist16Dev[16 - m]};
+#else
+  const double C[17] = TFB_TWIST16_VALUES;
+  return cd{C[m], C[16 - m]};
+#endif
+}
+
+// ---- 16-point DFT in registers: X[k] = sum_m x[m] exp(SIGN 2 pi i m k / 16), natural order ----
+template <int SIGN>
+TFB_HD void dft4(cd& z0, cd& z1, cd& z2, cd& z3) {
+  const cd t0 = cadd(z0, z2), t1 = csub(z0, z2), t2 = cadd(z1, z3), t3 = mul_i<SIGN>(csub(z1, z3));
+  z0 = cadd(t0, t2);
+  z1 = cadd(t1, t3);
+  z2 = csub(t0, t2);
+  z3 = csub(t1, t3);
+}
+
+template <int SIGN>
+TFB_HD cd mul_w16(cd v, int e) {  // v * exp(SIGN 2 pi i e / 16), e a compile-time constant after unrolling
+  const double c1 = 0.9238795325112867, s1 = 0.3826834323650898, h = 0.7071067811865476;
+  const double CO[10] = {1.0, c1, h, s1, 0.0, -s1, -h, -c1, -1.0, -c1};
+  const double SI[10] = {0.0, s1, h, c1, 1.0, c1, h, s1, 0.0, -s1};
+  if (e == 0) return v;
+  if (e == 4) return mul_i<SIGN>(v);
+  return cmul(v, cd{CO[e], SIGN * SI[e]});
+}
+
+template <int SIGN>
+TFB_HD void dft16(cd* x) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a) dft4<SIGN>(x[a], x[a + 4], x[a + 8], x[a + 12]);
+    // x[a + 4 k0] = y_a[k0]; twiddle w16^{a k0}
+#pragma unroll
+  for (int a = 1; a < 4; ++a)
+#pragma unroll
+    for (int k0 = 1; k0 < 4; ++k0) x[a + 4 * k0] = mul_w16<SIGN>(x[a + 4 * k0], a * k0);
+#pragma unroll
+  for (int k0 = 0; k0 < 4; ++k0) dft4<SIGN>(x[4 * k0], x[4 * k0 + 1], x[4 * k0 + 2], x[4 * k0 + 3]);
+    // x[k1 + 4 k0] = X[k0 + 4 k1]: transpose to natural order (register renaming)
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = i + 1; j < 4; ++j) {
+      const cd tmp = x[i + 4 * j];
+      x[i + 4 * j] = x[j + 4 * i];
+      x[j + 4 * i] = tmp;
+    }
+}
+
+// Exchange buffer slot of U[r][k1][b]; the XOR makes the accesses of both sides (fixed (k1, b)
+// over consecutive r; fixed r over consecutive k1) bank-conflict-free for 16-byte and for
+// 8-byte elements.
+TFB_HD int wslot(int r, int k1, int b) { return 32 * r + ((k1 + 16 * b) ^ (r & 15)); }
+
+// Spectral index held by (lane t, register q) after wfft_forward.
+TFB_HD int wspectral_index(int t, int q) { return (t & 15) + 16 * (2 * q + (t >> 4)); }
+
+// The one shared-memory exchange of a transform.  Before it lane (r, h) = (t & 15, t >> 4)
+// holds U[r][8h + j][b] in register 8b + j; after it lane (k1, b) = (t & 15, t >> 4) holds
+// U[r][k1][b] in register r (FWD), or the other way round (inverse).  SPLIT moves the real and
+// the imaginary parts in two rounds through a buffer of 512 doubles (4 KB per warp instead of
+// 8 KB: room for more warps per SM).
+#ifndef TFB_K1D_SPLIT
+#define TFB_K1D_SPLIT 1
+#endif
+constexpr bool WX_SPLIT = TFB_K1D_SPLIT != 0;
+constexpr int WBUF_BYTES = HALF_N * (WX_SPLIT ? 8 : 16);
+
+template <bool FWD>
+TFB_HD int wx_src(int t, int k) {  // slot of register k on the side that holds (r, h)-ordered data
+  return wslot(t & 15, 8 * (t >> 4) + (k & 7), k >> 3);
+}
+TFB_HD int wx_dst(int t, int k) { return wslot(k, t & 15, t >> 4); }  // (k1, b)-ordered side, register k = r
+
+template <bool FWD, class W>
+TFB_HD void wexchange(cd* x, int t, void* buf, W& w) {
+  if (WX_SPLIT) {
+    double* b = reinterpret_cast<double*>(buf);
+#pragma unroll
+    for (int k = 0; k < WPTS; ++k) b[FWD ? wx_src<FWD>(t, k) : wx_dst(t, k)] = x[k].re;
+    w();
+#pragma unroll
+    for (int k = 0; k < WPTS; ++k) x[k].re = b[FWD ? wx_dst(t, k) : wx_src<FWD>(t, k)];
+    w();
+#pragma unroll
+    for (int k = 0; k < WPTS; ++k) b[FWD ? wx_src<FWD>(t, k) : wx_dst(t, k)] = x[k].im;
+    w();
+#pragma unroll
+    for (int k = 0; k < WPTS; ++k) x[k].im = b[FWD ? wx_dst(t, k) : wx_src<FWD>(t, k)];
+    w();  // the buffer may be overwritten by the next transform
+  } else {
+    cd* b = reinterpret_cast<cd*>(buf);
+#pragma unroll
+    for (int k = 0; k < WPTS; ++k) b[FWD ? wx_src<FWD>(t, k) : wx_dst(t, k)] = x[k];
+    w();
+#pragma unroll
+    for (int k = 0; k < WPTS; ++k) x[k] = b[FWD ? wx_dst(t, k) : wx_src<FWD>(t, k)];
+    w();
+  }
+}
+
+// flip the sign of x[m], odd m, on the lanes with h = 1 (sgn = h << 31): multiplying the
+// inputs of a 16-point DFT by (-1)^m rotates its outputs by 8
+TFB_HD void wflip_odd(cd* x, uint32_t sgn) {
+#pragma unroll
+  for (int m = 1; m < WPTS; m += 2) {
+    x[m].re = bits_to_double(double_to_bits(x[m].re) ^ ((uint64_t)sgn << 32));
+    x[m].im = bits_to_double(double_to_bits(x[m].im) ^ ((uint64_t)sgn << 32));
+  }
+}
+
+// W: warp primitives -- operator()() = warp barrier with memory ordering, xchg16(v) = the
+// value lane (t ^ 16) passed.
+//
+// Forward negacyclic transform, unnormalised, 512 = 16 x 2 x 16:
+//   pass 1   16-point DFTs over m of x[t + 32 m] in registers, twiddle W512^{t k1};
+//   radix 2  between lanes t and t ^ 16 (decimation in frequency: butterfly, then the twiddle
+//            W32^{r} on the odd half), 8 values sent and 8 received per lane.  Lane h = 1
+//            keeps frequencies 8..15 and sends 0..7, lane h = 0 the opposite; to keep the code
+//            free of selects lane h = 1 runs pass 1 with its odd inputs negated, which leaves
+//            frequency k ^ 8 in register k, and carries the sign of its (K - G) in c[t];
+//   exchange through shared memory, then 16-point DFTs over r.
+//   in : x[m] = c_{t+32m} = a_{t+32m} + i a_{t+32m+512}   (untwisted)
+//   out: x[q] = Z[wspectral_index(t, q)],  Z_k = sum_j c_j exp(i pi j / N) exp(2 pi i j k / 512)
+// buf: WBUF_BYTES of shared memory private to the warp.
+template <class W>
+TFB_HD void wfft_forward(cd* x, int t, const WarpTwiddles* tw, void* buf, W& w) {
+  wflip_odd(x, (uint32_t)(t >> 4) << 31);
+#pragma unroll
+  for (int m = 1; m < WPTS; ++m) x[m] = cmul(x[m], twist16(m));
+  dft16<1>(x);
+  {
+    const cd g = tw->g[t];
+    cd wa = tw->sa[t], wb = tw->sb[t];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      x[j] = cmul(x[j], wa);
+      x[8 + j] = cmul(x[8 + j], wb);
+      if (j < 7) {
+        wa = cmul(wa, g);
+        wb = cmul(wb, g);
+      }
+    }
+  }
+  {
+    const cd c = tw->c[t];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const cd got = w.xchg16(x[8 + j]);
+      const cd u0 = cadd(x[j], got), u1 = csub(x[j], got);
+      x[j] = u0;
+      x[8 + j] = cmul(u1, c);
+    }
+  }
+  wexchange<true>(x, t, buf, w);
+  dft16<1>(x);
+}
+
+// Inverse of wfft_forward up to the factor 512 (folded into the key): the conjugate transpose,
+// stage by stage.
+//   in : x[q] = S[wspectral_index(t, q)]
+//   out: x[m] = c_{t+32m}  (re -> coefficient t+32m, im -> coefficient t+32m+512)
+template <class W>
+TFB_HD void wfft_inverse(cd* x, int t, const WarpTwiddles* tw, void* buf, W& w) {
+  dft16<-1>(x);
+  wexchange<false>(x, t, buf, w);
+  {
+    const cd c = tw->c[t];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const cd v = cmulc(x[8 + j], c);
+      const cd keep = cadd(x[j], v);
+      x[8 + j] = w.xchg16(csub(x[j], v));
+      x[j] = keep;
+    }
+  }
+  {
+    const cd g = tw->g[t];
+    cd wa = tw->sa[t], wb = tw->sb[t];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      x[j] = cmulc(x[j], wa);
+      x[8 + j] = cmulc(x[8 + j], wb);
+      if (j < 7) {
+        wa = cmul(wa, g);
+        wb = cmul(wb, g);
+      }
+    }
+  }
+  dft16<-1>(x);
+#pragma unroll
+  for (int m = 1; m < WPTS; ++m) x[m] = cmulc(x[m], twist16(m));
+  wflip_odd(x, (uint32_t)(t >> 4) << 31);
+}
+
+// Spectral key stage (i, p) in this kernel's order: [lvl][q][c][lane], prescaled by 1/512
+// (same 32 KB per stage and the same stage_offset as the 64-thread layout).
+TFB_HD int wstage_index(int lvl, int q, int c, int t) { return ((lvl * WPTS + q) * 2 + c) * WARP_T + t; }
+
+// Accumulator parking.  The 2 x 16 complex accumulators of a CMux are idle while a transform
+// runs; a Park policy holds them outside the register file between MAC stages (the B200 kernel
+// parks them in tensor memory, which is private per lane and has its own data path), in
+// chunks of PARK_CH values per output polynomial:
+//   load(qb, o0, o1) / store(qb, o0, o1): values qb .. qb+PARK_CH-1 of both polynomials
+//   load_one(c, qb, o): the same of polynomial c only;  flush(): stores are visible to later loads
+//   store_digits / load_digits: the 16 packed level-1 digit words that wait for the second
+//   forward transform of an accumulator polynomial
+#ifndef TFB_PARK_CH
+#define TFB_PARK_CH 4
+#endif
+constexpr int PARK_CH = TFB_PARK_CH;
+struct RegPark {  // no parking: plain registers (host emulation)
+  cd v[2][WPTS];
+  TFB_HD void load_one(int c, int qb, cd* o) const {
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j) o[j] = v[c][qb + j];
+  }
+  TFB_HD void load(int qb, cd* o0, cd* o1) const {
+    load_one(0, qb, o0);
+    load_one(1, qb, o1);
+  }
+  TFB_HD void store(int qb, const cd* o0, const cd* o1) {
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j) {
+      v[0][qb + j] = o0[j];
+      v[1][qb + j] = o1[j];
+    }
+  }
+  TFB_HD void flush() const {}
+  uint32_t d[WPTS];
+  TFB_HD void store_digits(const uint32_t* v) {
+#pragma unroll
+    for (int m = 0; m < WPTS; ++m) d[m] = v[m];
+  }
+  TFB_HD void load_digits(uint32_t* v) const {
+#pragma unroll
+    for (int m = 0; m < WPTS; ++m) v[m] = d[m];
+  }
+};
+
+// MAC of one forward-transformed digit polynomial x against level `lvl` of the staged key;
+// the accumulators live in the park.  FIRST starts them instead of loading them.
+template <bool FIRST, class BkSource, class Park>
+TFB_HD void wmac(Park& park, const cd* x, BkSource& bk, const cd* stage, int lvl, int t) {
+  const cd* key = stage + wstage_index(lvl, 0, 0, t);
+#pragma unroll
+  for (int qb = 0; qb < WPTS; qb += PARK_CH) {
+    cd o0[PARK_CH], o1[PARK_CH];
+    if (!FIRST) park.load(qb, o0, o1);
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j) {
+      const int q = qb + j;
+      const cd b0 = bk.load(key + wstage_index(0, q, 0, 0)), b1 = bk.load(key + wstage_index(0, q, 1, 0));
+      if (FIRST) {
+        o0[j] = cmul(x[q], b0);
+        o1[j] = cmul(x[q], b1);
+      } else {
+        cmac(o0[j], x[q], b0);
+        cmac(o1[j], x[q], b1);
+      }
+    }
+    park.store(qb, o0, o1);
+  }
+  park.flush();
+}
+
+// Stage s = 2p + lvl of a CMux: digits of accumulator polynomial p at gadget level lvl (read
+// and decomposed from ACC for lvl 0, which also parks the level-1 digit words; taken from the
+// park for lvl 1), forward transform, MAC against the key.
+template <bool FIRST, class W, class BkSource, class Park>
+TFB_HD void wcmux_stage(int s, const cd*& stage, const uint32_t* acc, int abar, int i, BkSource& bk, int t,
+                        const WarpTwiddles* tw, void* buf, W& w, Park& park) {
+  const int p = s >> 1, lvl = s & 1;
+  cd x[WPTS];
+  uint32_t d1[WPTS];  // level-1 digit fields of (re, im), 16 bits each
+  if (lvl == 0) {
+    // The rotation indices depend only on (abar, lane); hidden behind an opaque copy the
+    // compiler recomputes them here instead of carrying 64 of them across the whole CMux.
+    int rot = abar;
+    TFB_OPAQUE(rot);
+#pragma unroll
+    for (int m = 0; m < WPTS; ++m) {
+      const uint32_t vr = rotated_diff(acc + p * RING_N, t + 32 * m, rot) + DECOMP_OFFSET;
+      const uint32_t vi = rotated_diff(acc + p * RING_N, t + 32 * m + HALF_N, rot) + DECOMP_OFFSET;
+      x[m] = cd{digit_to_double(digit_field(vr, 0)), digit_to_double(digit_field(vi, 0))};
+      d1[m] = digit_field(vr, 1) | (digit_field(vi, 1) << 16);
+    }
+    park.store_digits(d1);
+  } else {
+    park.load_digits(d1);
+#pragma unroll
+    for (int m = 0; m < WPTS; ++m) x[m] = cd{digit_to_double(d1[m] & 0xffffu), digit_to_double(d1[m] >> 16)};
+  }
+  wfft_forward(x, t, tw, buf, w);
+  if (lvl == 0) stage = bk.acquire(i, p);
+  wmac<FIRST>(park, x, bk, stage, lvl, t);
+  if (lvl == 1) bk.release();
+}
+
+// One CMux step by one warp.  acc: 2 polynomials of N words in shared memory.
+// Stage 0 starts the accumulators; stages 1..3 and the two inverse transforms run as rolled
+// loops (TFB_K1D_ROLL): one copy of the transform code in the instruction cache.
+template <class W, class BkSource, class Park>
+TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, const WarpTwiddles* tw, void* buf,
+                       W& w, Park& park) {
+  const cd* stage = nullptr;
+  wcmux_stage<true>(0, stage, acc, abar, i, bk, t, tw, buf, w, park);
+  TFB_K1D_LOOP
+  for (int s = 1; s < 4; ++s) wcmux_stage<false>(s, stage, acc, abar, i, bk, t, tw, buf, w, park);
+  TFB_K1D_LOOP
+  for (int c = 0; c < 2; ++c) {
+    cd x[WPTS];
+#pragma unroll
+    for (int qb = 0; qb < WPTS; qb += PARK_CH) park.load_one(c, qb, x + qb);
+    wfft_inverse(x, t, tw, buf, w);
+#pragma unroll
+    for (int m = 0; m < WPTS; ++m) {
+      acc[c * RING_N + t + 32 * m] += round_to_word(x[m].re);
+      acc[c * RING_N + t + 32 * m + HALF_N] += round_to_word(x[m].im);
+    }
+  }
+  w();
+}
+
+// Whole gate bootstrap (without key switch) for one ciphertext by one warp.
+//   sm_acc: 2N words, sm_abar: n+1 uint16, buf: WBUF_BYTES, ext: N+1 words out
+template <class W, class BkSource, class Park>
+TFB_HD void gate_bootstrap_warp(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu,
+                                BkSource& bk, const WarpTwiddles* tw, uint32_t* sm_acc, uint16_t* sm_abar,
+                                void* buf, uint32_t* ext, int t, W& w, Park& park) {
+  bootstrap_prologue(x_row, y_row, kind, n, mu, sm_acc, sm_abar, t, WARP_T, w);
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    const int abar = sm_abar[i];
+    if (abar == 0) {  // uniform across the warp
+      bk.skip(i);
+      continue;
+    }
+    wcmux_step(sm_acc, abar, i, bk, t, tw, buf, w, park);
+  }
+  if (ext) bootstrap_extract(sm_acc, ext, t, WARP_T);  // null: surplus warp of a tail CTA
+}
+
+}  // namespace tfb

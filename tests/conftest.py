@@ -59,9 +59,9 @@ def emu_lib():
     import ctypes
 
     src = os.path.join(ROOT, "tests", "emu", "emu_bootstrap.cpp")
-    hdr = os.path.join(ROOT, "paper_2005_01945_b200", "csrc", "tfhe_device.cuh")
+    hdrs = [os.path.join(ROOT, "paper_2005_01945_b200", "csrc", h) for h in ("tfhe_device.cuh", "tfhe_warp.cuh")]
     so = os.path.join(ROOT, "tests", "emu", "libtfhe_emu.so")
-    if not os.path.exists(so) or os.path.getmtime(so) < max(os.path.getmtime(src), os.path.getmtime(hdr)):
+    if not os.path.exists(so) or os.path.getmtime(so) < max(os.path.getmtime(f) for f in [src, *hdrs]):
         subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", "-o", so, src])
     return ctypes.CDLL(so)
 

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../paper_2005_01945_b200/csrc/tfhe_device.cuh"
+#include "../../paper_2005_01945_b200/csrc/tfhe_warp.cuh"
 
 using namespace tfb;
 
@@ -164,5 +165,117 @@ void emu_ks_digits(const uint32_t* ext, int32_t* digits_out) {
   const uint32_t bias = ks_bias();
   for (int i = 0; i < RING_N; ++i)
     for (int j = 0; j < KS_T; ++j) digits_out[i * KS_T + j] = ks_digit(ext[i] + bias, j);
+}
+}
+
+// ---- K1d: one ciphertext per warp (tfhe_warp.cuh), 32 host threads per warp ----------------
+namespace {
+struct EmuWarp {
+  pthread_barrier_t* b;
+  cd* scratch;  // 32 cd
+  int lane;
+  void operator()() const { pthread_barrier_wait(b); }
+  cd xchg16(cd v) const {
+    scratch[lane] = v;
+    pthread_barrier_wait(b);
+    const cd r = scratch[lane ^ 16];
+    pthread_barrier_wait(b);
+    return r;
+  }
+};
+
+void fill_warp_twiddles(WarpTwiddles* tw) { tfb::fill_warp_twiddles<long double>(tw, cosl, sinl); }
+
+template <class F>
+void run_warp(F body) {
+  pthread_barrier_t bar;
+  pthread_barrier_init(&bar, nullptr, WARP_T);
+  std::vector<cd> scratch(WARP_T);
+  std::vector<std::thread> th;
+  for (int t = 0; t < WARP_T; ++t)
+    th.emplace_back([&, t] {
+      EmuWarp w{&bar, scratch.data(), t};
+      body(t, w);
+    });
+  for (auto& x : th) x.join();
+  pthread_barrier_destroy(&bar);
+}
+}  // namespace
+
+extern "C" {
+
+void emu_w_fft_forward(const int32_t* poly, double* spec_out) {
+  WarpTwiddles tw;
+  fill_warp_twiddles(&tw);
+  std::vector<cd> buf(HALF_N);
+  cd* out = reinterpret_cast<cd*>(spec_out);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(poly);
+  run_warp([&](int t, EmuWarp& w) {
+    cd x[WPTS];
+    for (int m = 0; m < WPTS; ++m)
+      x[m] = cd{int32_to_double(src[t + 32 * m]), int32_to_double(src[t + 32 * m + HALF_N])};
+    wfft_forward(x, t, &tw, buf.data(), w);
+    for (int q = 0; q < WPTS; ++q) out[wspectral_index(t, q)] = x[q];
+  });
+}
+
+void emu_w_fft_inverse(const double* spec_in, uint32_t* poly_out) {
+  WarpTwiddles tw;
+  fill_warp_twiddles(&tw);
+  std::vector<cd> buf(HALF_N);
+  const cd* in = reinterpret_cast<const cd*>(spec_in);
+  run_warp([&](int t, EmuWarp& w) {
+    cd x[WPTS];
+    for (int q = 0; q < WPTS; ++q) {
+      const cd v = in[wspectral_index(t, q)];
+      x[q] = cd{v.re / HALF_N, v.im / HALF_N};
+    }
+    wfft_inverse(x, t, &tw, buf.data(), w);
+    for (int m = 0; m < WPTS; ++m) {
+      poly_out[t + 32 * m] = round_to_word(x[m].re);
+      poly_out[t + 32 * m + HALF_N] = round_to_word(x[m].im);
+    }
+  });
+}
+
+// spectral key in K1d's staged layout [n][p][lvl][q][c][lane], prescaled by 1/512
+void emu_w_bk_transform(const int32_t* bk_raw, int n, double* bkf_out) {
+  WarpTwiddles tw;
+  fill_warp_twiddles(&tw);
+  cd* bkf = reinterpret_cast<cd*>(bkf_out);
+  std::vector<cd> buf(HALF_N);
+  for (int64_t poly = 0; poly < (int64_t)n * BK_ROWS * 2; ++poly) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(bk_raw) + poly * RING_N;
+    const int c = (int)(poly & 1);
+    const int64_t ir = poly >> 1;
+    run_warp([&](int t, EmuWarp& w) {
+      cd x[WPTS];
+      for (int m = 0; m < WPTS; ++m)
+        x[m] = cd{int32_to_double(src[t + 32 * m]), int32_to_double(src[t + 32 * m + HALF_N])};
+      wfft_forward(x, t, &tw, buf.data(), w);
+      for (int q = 0; q < WPTS; ++q)
+        bkf[stage_offset((int)(ir / BK_ROWS), (int)(ir % BK_ROWS) / BK_L) + wstage_index((int)(ir % BK_L), q, c, t)] =
+            cd{x[q].re / HALF_N, x[q].im / HALF_N};
+    });
+  }
+}
+
+void emu_w_gate_bootstrap(const uint32_t* x, const uint32_t* y, const uint8_t* kinds, int64_t k, int n,
+                          uint32_t mu, const double* bkf_in, uint32_t* ext_out) {
+  WarpTwiddles tw;
+  fill_warp_twiddles(&tw);
+  const cd* bkf = reinterpret_cast<const cd*>(bkf_in);
+  for (int64_t g = 0; g < k; ++g) {
+    std::vector<cd> buf(HALF_N);
+    std::vector<uint32_t> acc(2 * RING_N), ext(EXT_STRIDE);
+    std::vector<uint16_t> abar(n + 1);
+    run_warp([&](int t, EmuWarp& w) {
+      GlobalBk bk{bkf};
+      RegPark park;
+      gate_bootstrap_warp(x + g * (n + 1), y + g * (n + 1), (int)kinds[g], n, mu, bk, &tw, acc.data(),
+                          abar.data(), buf.data(), ext.data(), t, w, park);
+    });
+    for (int j = 0; j <= RING_N; ++j) ext_out[g * (RING_N + 1) + j] = ext[j];
+  }
 }
 }

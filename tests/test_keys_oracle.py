@@ -174,6 +174,13 @@ def test_kernel_arithmetic_on_host_threads_matches_oracle(emu_lib, key):
     emu_lib.emu_gate_bootstrap_wide(vp(xs.ctypes.data), vp(ys.ctypes.data), vp(kinds.ctypes.data), ctypes.c_int64(K),
                                     n, ctypes.c_uint32(p.mu.word), vp(bkf.ctypes.data), vp(wide.ctypes.data))
     assert np.array_equal(wide, ext)
+    # K1d (one ciphertext per warp, radix-16 transforms, its own spectral key order)
+    bkw = np.empty((n, 2, 2, 16, 2, 32, 2), dtype=np.float64)
+    emu_lib.emu_w_bk_transform(vp(ek.bk.ctypes.data), n, vp(bkw.ctypes.data))
+    warp = np.empty((K, 1025), dtype=np.uint32)
+    emu_lib.emu_w_gate_bootstrap(vp(xs.ctypes.data), vp(ys.ctypes.data), vp(kinds.ctypes.data), ctypes.c_int64(K), n,
+                                 ctypes.c_uint32(p.mu.word), vp(bkw.ctypes.data), vp(warp.ctypes.data))
+    assert np.array_equal(warp, ext)
     # K2's digit extraction against the oracle's key switch
     digits = np.empty((1024, 8), dtype=np.int32)
     emu_lib.emu_ks_digits(vp(ext[0].ctypes.data), vp(digits.ctypes.data))
@@ -196,3 +203,11 @@ def test_kernel_fft_roundtrip_and_spectrum(emu_lib):
     back = np.empty(1024, dtype=np.uint32)
     emu_lib.emu_fft_inverse(vp(spec.ctypes.data), vp(back.ctypes.data))
     assert np.array_equal(back.view(np.int32), poly)
+    # the warp-level transform of K1d (16 points per lane, one exchange + one shuffle stage)
+    spec_w = np.empty((512, 2), dtype=np.float64)
+    emu_lib.emu_w_fft_forward(vp(poly.ctypes.data), vp(spec_w.ctypes.data))
+    got_w = spec_w[:, 0] + 1j * spec_w[:, 1]
+    assert np.abs(got_w - want).max() / np.abs(want).max() < 1e-14
+    back_w = np.empty(1024, dtype=np.uint32)
+    emu_lib.emu_w_fft_inverse(vp(spec_w.ctypes.data), vp(back_w.ctypes.data))
+    assert np.array_equal(back_w.view(np.int32), poly)
