@@ -530,6 +530,52 @@ struct TmemWPark {
   }
 };
 constexpr uint32_t K1D_TMEM_SLICE = 144;  // columns per warp: 2 x 64 accumulators + 16 digit words
+constexpr uint32_t K1D_TMEM_TW = ((K1D_WARPS + 3) / 4) * K1D_TMEM_SLICE;  // first column of the twiddle table
+constexpr uint32_t K1D_TMEM_NEED = K1D_TMEM_TW + 68;                      // 16 twiddles + c per lane
+
+// Per-lane twiddle table in tensor memory (shared by the warps of a lane quarter): 16 pass-1
+// twiddles at columns 4k .. 4k+3, the radix-2 twiddle at columns 64 .. 67.
+struct TmemTw {
+  uint32_t taddr;  // (lane << 16) | first column of the table
+  __device__ __forceinline__ void get4(int kb, cd* w) const {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];\n\ttcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr + 4 * kb)
+        : "memory");
+    TmemWPark::unpack(r, w);
+  }
+  __device__ __forceinline__ cd cc() const {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n\ttcgen05.wait::ld.sync.aligned;"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr + 64)
+                 : "memory");
+    return cd{__hiloint2double((int)r[1], (int)r[0]), __hiloint2double((int)r[3], (int)r[2])};
+  }
+  // one warp per lane quarter writes the table
+  __device__ __forceinline__ void fill(const LaneTwiddles& lt) const {
+#pragma unroll
+    for (int kb = 0; kb < WPTS; kb += 4) {
+      uint32_t r[16];
+      TmemWPark::pack(lt.w + kb, r);
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+          "%15, %16};" ::"r"(taddr + 4 * kb),
+          "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+          "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+          : "memory");
+    }
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + 64),
+                 "r"((uint32_t)__double2loint(lt.c.re)), "r"((uint32_t)__double2hiint(lt.c.re)),
+                 "r"((uint32_t)__double2loint(lt.c.im)), "r"((uint32_t)__double2hiint(lt.c.im))
+                 : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+};
 
 __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
@@ -558,9 +604,9 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   // tensor memory: one slice per warp, warps w, w+4, w+8 share a lane quarter
-  constexpr uint32_t kTmemNeed = ((K1D_WARPS + 3) / 4) * K1D_TMEM_SLICE;
-  constexpr uint32_t kTmemCols = kTmemNeed <= 128 ? 128 : (kTmemNeed <= 256 ? 256 : 512);
-  static_assert(kTmemNeed <= 512, "tensor memory has 512 columns");
+  constexpr uint32_t kTmemCols = K1D_TMEM_NEED <= 128 ? 128 : (K1D_TMEM_NEED <= 256 ? 256 : 512);
+  static_assert(K1D_TMEM_NEED <= 512, "tensor memory has 512 columns");
+  static_assert(PARK_CH == 4, "the tensor-memory helpers move 16 columns = 4 complex values at a time");
   __shared__ uint32_t tmem_base;
   if (wid == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
@@ -573,6 +619,15 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (threadIdx.x == 0)
     for (int j = 0; j < K1B_SLOTS; ++j) bk.issue(j);
+  const TmemTw ttw{tmem_base + ((((uint32_t)wid & 3u) * 32u) << 16) + K1D_TMEM_TW};
+  if (wid < 4) {  // one warp per lane quarter builds the twiddle table
+    LaneTwiddles lt;
+    build_lane_twiddles(tw, t, &lt);
+    ttw.fill(lt);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // tail CTA: surplus warps redo the last ciphertext (keeps the ring protocol uniform) but do not store
   const int64_t want = (int64_t)blockIdx.x * K1D_WARPS + wid;
   const int64_t g = want < k ? want : k - 1;
@@ -585,7 +640,7 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
 #else
   RegPark park;
 #endif
-  gate_bootstrap_warp(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, buf, dst, t, w, park);
+  gate_bootstrap_warp(xr, yr, (int)kinds[g], n, mu, bk, ttw, acc, abar, buf, dst, t, w, park);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (wid == 0)
@@ -715,7 +770,9 @@ __global__ void __launch_bounds__(WARP_T) k_bk_transform_w(const int32_t* __rest
   for (int m = 0; m < WPTS; ++m)
     x[m] = cd{int32_to_double(src[t + 32 * m]), int32_to_double(src[t + 32 * m + HALF_N])};
   DevWarp w;
-  wfft_forward(x, t, tw, buf, w);
+  LaneTwiddles lt;
+  build_lane_twiddles(tw, t, &lt);
+  wfft_forward(x, t, MemTw{&lt}, buf, w);
   const double scale = 1.0 / HALF_N;
 #pragma unroll
   for (int q = 0; q < WPTS; ++q)

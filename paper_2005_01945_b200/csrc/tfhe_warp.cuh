@@ -179,6 +179,37 @@ TFB_HD void wexchange(cd* x, int t, void* buf, W& w) {
   }
 }
 
+// The 16 pass-1 twiddles of a lane in register order (0..7 from sa, 8..15 from sb, each times
+// g, g^2, ...) and the radix-2 twiddle c.  Built once per lane; a twiddle provider hands them
+// to the transforms in chunks of four:
+//   get4(kb, w): twiddles kb .. kb+3;   cc(): the radix-2 twiddle
+// (the B200 kernel keeps the table in tensor memory: rebuilding the chain inside every
+// transform costs 56 FP64 instructions per transform on the pipe that limits K1d).
+struct LaneTwiddles {
+  cd w[WPTS];
+  cd c;
+};
+TFB_HD void build_lane_twiddles(const WarpTwiddles* tw, int t, LaneTwiddles* out) {
+  const cd g = tw->g[t];
+  cd wa = tw->sa[t], wb = tw->sb[t];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    out->w[j] = wa;
+    out->w[8 + j] = wb;
+    wa = cmul(wa, g);
+    wb = cmul(wb, g);
+  }
+  out->c = tw->c[t];
+}
+struct MemTw {  // table in addressable memory (host emulation, key setup kernel)
+  const LaneTwiddles* lt;
+  TFB_HD void get4(int kb, cd* w) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = lt->w[kb + j];
+  }
+  TFB_HD cd cc() const { return lt->c; }
+};
+
 // flip the sign of x[m], odd m, on the lanes with h = 1 (sgn = h << 31): multiplying the
 // inputs of a 16-point DFT by (-1)^m rotates its outputs by 8
 TFB_HD void wflip_odd(cd* x, uint32_t sgn) {
@@ -203,27 +234,21 @@ TFB_HD void wflip_odd(cd* x, uint32_t sgn) {
 //   in : x[m] = c_{t+32m} = a_{t+32m} + i a_{t+32m+512}   (untwisted)
 //   out: x[q] = Z[wspectral_index(t, q)],  Z_k = sum_j c_j exp(i pi j / N) exp(2 pi i j k / 512)
 // buf: WBUF_BYTES of shared memory private to the warp.
-template <class W>
-TFB_HD void wfft_forward(cd* x, int t, const WarpTwiddles* tw, void* buf, W& w) {
+template <class W, class Tw>
+TFB_HD void wfft_forward(cd* x, int t, const Tw& tw, void* buf, W& w) {
   wflip_odd(x, (uint32_t)(t >> 4) << 31);
 #pragma unroll
   for (int m = 1; m < WPTS; ++m) x[m] = cmul(x[m], twist16(m));
   dft16<1>(x);
-  {
-    const cd g = tw->g[t];
-    cd wa = tw->sa[t], wb = tw->sb[t];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      x[j] = cmul(x[j], wa);
-      x[8 + j] = cmul(x[8 + j], wb);
-      if (j < 7) {
-        wa = cmul(wa, g);
-        wb = cmul(wb, g);
-      }
-    }
+  for (int kb = 0; kb < WPTS; kb += 4) {
+    cd wk[4];
+    tw.get4(kb, wk);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[kb + j] = cmul(x[kb + j], wk[j]);
   }
   {
-    const cd c = tw->c[t];
+    const cd c = tw.cc();
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const cd got = w.xchg16(x[8 + j]);
@@ -240,12 +265,12 @@ TFB_HD void wfft_forward(cd* x, int t, const WarpTwiddles* tw, void* buf, W& w) 
 // stage by stage.
 //   in : x[q] = S[wspectral_index(t, q)]
 //   out: x[m] = c_{t+32m}  (re -> coefficient t+32m, im -> coefficient t+32m+512)
-template <class W>
-TFB_HD void wfft_inverse(cd* x, int t, const WarpTwiddles* tw, void* buf, W& w) {
+template <class W, class Tw>
+TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
   dft16<-1>(x);
   wexchange<false>(x, t, buf, w);
   {
-    const cd c = tw->c[t];
+    const cd c = tw.cc();
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const cd v = cmulc(x[8 + j], c);
@@ -254,18 +279,12 @@ TFB_HD void wfft_inverse(cd* x, int t, const WarpTwiddles* tw, void* buf, W& w) 
       x[j] = keep;
     }
   }
-  {
-    const cd g = tw->g[t];
-    cd wa = tw->sa[t], wb = tw->sb[t];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      x[j] = cmulc(x[j], wa);
-      x[8 + j] = cmulc(x[8 + j], wb);
-      if (j < 7) {
-        wa = cmul(wa, g);
-        wb = cmul(wb, g);
-      }
-    }
+  for (int kb = 0; kb < WPTS; kb += 4) {
+    cd wk[4];
+    tw.get4(kb, wk);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[kb + j] = cmulc(x[kb + j], wk[j]);
   }
   dft16<-1>(x);
 #pragma unroll
@@ -344,12 +363,26 @@ TFB_HD void wmac(Park& park, const cd* x, BkSource& bk, const cd* stage, int lvl
   park.flush();
 }
 
+// 10-bit digit field -> exact double of the signed digit.  TFB_K1D_I2F: integer conversion
+// instruction (one I2F on the conversion unit) instead of the mantissa trick of
+// digit_to_double (LOP3 + MOV + one DADD on the FP64 pipe, which K1d saturates first).
+#ifndef TFB_K1D_I2F
+#define TFB_K1D_I2F 0  // measured: 79.7 ms vs 78.0 ms per 14208 gates, the conversion is the slower one
+#endif
+TFB_HD double wdigit(uint32_t field) {
+#if defined(__CUDA_ARCH__) && TFB_K1D_I2F
+  return __int2double_rn((int)field - 512);
+#else
+  return digit_to_double(field);
+#endif
+}
+
 // Stage s = 2p + lvl of a CMux: digits of accumulator polynomial p at gadget level lvl (read
 // and decomposed from ACC for lvl 0, which also parks the level-1 digit words; taken from the
 // park for lvl 1), forward transform, MAC against the key.
-template <bool FIRST, class W, class BkSource, class Park>
+template <bool FIRST, class W, class BkSource, class Park, class Tw>
 TFB_HD void wcmux_stage(int s, const cd*& stage, const uint32_t* acc, int abar, int i, BkSource& bk, int t,
-                        const WarpTwiddles* tw, void* buf, W& w, Park& park) {
+                        const Tw& tw, void* buf, W& w, Park& park) {
   const int p = s >> 1, lvl = s & 1;
   cd x[WPTS];
   uint32_t d1[WPTS];  // level-1 digit fields of (re, im), 16 bits each
@@ -362,14 +395,14 @@ TFB_HD void wcmux_stage(int s, const cd*& stage, const uint32_t* acc, int abar, 
     for (int m = 0; m < WPTS; ++m) {
       const uint32_t vr = rotated_diff(acc + p * RING_N, t + 32 * m, rot) + DECOMP_OFFSET;
       const uint32_t vi = rotated_diff(acc + p * RING_N, t + 32 * m + HALF_N, rot) + DECOMP_OFFSET;
-      x[m] = cd{digit_to_double(digit_field(vr, 0)), digit_to_double(digit_field(vi, 0))};
+      x[m] = cd{wdigit(digit_field(vr, 0)), wdigit(digit_field(vi, 0))};
       d1[m] = digit_field(vr, 1) | (digit_field(vi, 1) << 16);
     }
     park.store_digits(d1);
   } else {
     park.load_digits(d1);
 #pragma unroll
-    for (int m = 0; m < WPTS; ++m) x[m] = cd{digit_to_double(d1[m] & 0xffffu), digit_to_double(d1[m] >> 16)};
+    for (int m = 0; m < WPTS; ++m) x[m] = cd{wdigit(d1[m] & 0xffffu), wdigit(d1[m] >> 16)};
   }
   wfft_forward(x, t, tw, buf, w);
   if (lvl == 0) stage = bk.acquire(i, p);
@@ -380,9 +413,9 @@ TFB_HD void wcmux_stage(int s, const cd*& stage, const uint32_t* acc, int abar, 
 // One CMux step by one warp.  acc: 2 polynomials of N words in shared memory.
 // Stage 0 starts the accumulators; stages 1..3 and the two inverse transforms run as rolled
 // loops (TFB_K1D_ROLL): one copy of the transform code in the instruction cache.
-template <class W, class BkSource, class Park>
-TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, const WarpTwiddles* tw, void* buf,
-                       W& w, Park& park) {
+template <class W, class BkSource, class Park, class Tw>
+TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, const Tw& tw, void* buf, W& w,
+                       Park& park) {
   const cd* stage = nullptr;
   wcmux_stage<true>(0, stage, acc, abar, i, bk, t, tw, buf, w, park);
   TFB_K1D_LOOP
@@ -404,9 +437,9 @@ TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, cons
 
 // Whole gate bootstrap (without key switch) for one ciphertext by one warp.
 //   sm_acc: 2N words, sm_abar: n+1 uint16, buf: WBUF_BYTES, ext: N+1 words out
-template <class W, class BkSource, class Park>
+template <class W, class BkSource, class Park, class Tw>
 TFB_HD void gate_bootstrap_warp(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu,
-                                BkSource& bk, const WarpTwiddles* tw, uint32_t* sm_acc, uint16_t* sm_abar,
+                                BkSource& bk, const Tw& tw, uint32_t* sm_acc, uint16_t* sm_abar,
                                 void* buf, uint32_t* ext, int t, W& w, Park& park) {
   bootstrap_prologue(x_row, y_row, kind, n, mu, sm_acc, sm_abar, t, WARP_T, w);
 #pragma unroll 1

@@ -214,7 +214,9 @@ void emu_w_fft_forward(const int32_t* poly, double* spec_out) {
     cd x[WPTS];
     for (int m = 0; m < WPTS; ++m)
       x[m] = cd{int32_to_double(src[t + 32 * m]), int32_to_double(src[t + 32 * m + HALF_N])};
-    wfft_forward(x, t, &tw, buf.data(), w);
+    LaneTwiddles lt;
+    build_lane_twiddles(&tw, t, &lt);
+    wfft_forward(x, t, MemTw{&lt}, buf.data(), w);
     for (int q = 0; q < WPTS; ++q) out[wspectral_index(t, q)] = x[q];
   });
 }
@@ -230,7 +232,9 @@ void emu_w_fft_inverse(const double* spec_in, uint32_t* poly_out) {
       const cd v = in[wspectral_index(t, q)];
       x[q] = cd{v.re / HALF_N, v.im / HALF_N};
     }
-    wfft_inverse(x, t, &tw, buf.data(), w);
+    LaneTwiddles lt;
+    build_lane_twiddles(&tw, t, &lt);
+    wfft_inverse(x, t, MemTw{&lt}, buf.data(), w);
     for (int m = 0; m < WPTS; ++m) {
       poly_out[t + 32 * m] = round_to_word(x[m].re);
       poly_out[t + 32 * m + HALF_N] = round_to_word(x[m].im);
@@ -252,7 +256,9 @@ void emu_w_bk_transform(const int32_t* bk_raw, int n, double* bkf_out) {
       cd x[WPTS];
       for (int m = 0; m < WPTS; ++m)
         x[m] = cd{int32_to_double(src[t + 32 * m]), int32_to_double(src[t + 32 * m + HALF_N])};
-      wfft_forward(x, t, &tw, buf.data(), w);
+      LaneTwiddles lt;
+      build_lane_twiddles(&tw, t, &lt);
+      wfft_forward(x, t, MemTw{&lt}, buf.data(), w);
       for (int q = 0; q < WPTS; ++q)
         bkf[stage_offset((int)(ir / BK_ROWS), (int)(ir % BK_ROWS) / BK_L) + wstage_index((int)(ir % BK_L), q, c, t)] =
             cd{x[q].re / HALF_N, x[q].im / HALF_N};
@@ -272,7 +278,9 @@ void emu_w_gate_bootstrap(const uint32_t* x, const uint32_t* y, const uint8_t* k
     run_warp([&](int t, EmuWarp& w) {
       GlobalBk bk{bkf};
       RegPark park;
-      gate_bootstrap_warp(x + g * (n + 1), y + g * (n + 1), (int)kinds[g], n, mu, bk, &tw, acc.data(),
+      LaneTwiddles lt;
+      build_lane_twiddles(&tw, t, &lt);
+      gate_bootstrap_warp(x + g * (n + 1), y + g * (n + 1), (int)kinds[g], n, mu, bk, MemTw{&lt}, acc.data(),
                           abar.data(), buf.data(), ext.data(), t, w, park);
     });
     for (int j = 0; j <= RING_N; ++j) ext_out[g * (RING_N + 1) + j] = ext[j];
