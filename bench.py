@@ -350,7 +350,7 @@ def run_b200(args) -> None:
         "gpu_launches": int(gpu_launches),
         "correct": correct,
         "roofline": {
-            "kernel": "k_gate_bootstrap_ring (fused linear form + blind rotation + sample extract)",
+            "kernel": "k_gate_bootstrap_warp (K1d: fused linear form + blind rotation + sample extract, one gate per warp)",
             "bound": "fp64", "achieved": k1_tflops, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
             "frac": k1_tflops / peaks["fp64_tflops"], "traffic": traffic,
             "flop_per_gate": FLOP_PER_GATE, "ms_per_launch": k1_ms, "share_of_step": k1_ms / (total_ms / args.steps),

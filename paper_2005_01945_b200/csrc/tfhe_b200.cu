@@ -33,7 +33,7 @@ static_assert(TFB_EXT_STRIDE == EXT_STRIDE, "header / device stride mismatch");
 // ------------------------------------------------------------------------------------
 // context
 // ------------------------------------------------------------------------------------
-constexpr int64_t HOST_CHUNK = 16384;  // gates per pipeline chunk of tfb_gate_launch_host
+constexpr int64_t HOST_CHUNK = 21312;  // gates per pipeline chunk of tfb_gate_launch_host: 12 full waves of K1d CTAs (148 SMs x 12 gates)
 constexpr int HOST_EVENTS = 8;         // event slots; a slot is reused 8 chunks later (long after it fired)
 
 struct tfb_ctx {
@@ -395,48 +395,87 @@ constexpr int K1D_THREADS = K1D_WARPS * WARP_T;
 __host__ __device__ constexpr int warp_smem(int n) {
   return WBUF_BYTES + 2 * RING_N * (int)sizeof(uint32_t) + ((n + 1) * 2 + 15) / 16 * 16;
 }
-constexpr int K1D_HEADER = (int)sizeof(WarpTwiddles) + K1B_SLOTS * STAGE_BYTES + 64;
+constexpr int K1D_HEADER = (int)sizeof(WarpTwiddles) + 4 * 16384 + 128;  // twiddles | key ring (WR_SLOTS x 16 KB <= 64 KB) | barriers
 
-// Key ring of K1d.  Consumers wait on the full mbarrier of a slot; a slot is handed back by
-// counting releases, and the warp whose release is the last one issues the bulk copy of the
-// stage that reuses the slot (no dedicated producer: with a fixed producer thread every warp
-// of the CTA is gated by that thread's own progress, and the others spin on the barrier).
+// Key ring of K1d: WR_SLOTS chunks of 16 KB (one (i, p, lvl): what one MAC consumes).
+// Consumers wait on the full mbarrier of a slot; a slot is handed back by counting releases,
+// and the warp whose release is the last one issues the bulk copy of the chunk that reuses
+// the slot (no dedicated producer: with a fixed producer thread every warp of the CTA is
+// gated by that thread's own progress).  A warp may run WR_SLOTS - 1 chunks ahead of the
+// slowest one before it has to wait.
+#ifndef TFB_K1D_SLOTS
+#define TFB_K1D_SLOTS 4
+#endif
+constexpr int WR_SLOTS = TFB_K1D_SLOTS;
+constexpr int WR_CHUNK_BYTES = WCHUNK_CD * (int)sizeof(cd);
+// Non-blocking poll + sleep: a warp that is ahead of the key ring should cost (almost) no issue
+// slots while it waits; the try_wait spin loop executed ~200 instructions per acquire.
+__device__ __forceinline__ bool mbar_test_u32(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  while (!mbar_test_u32(bar, parity)) __nanosleep(100);
+}
 struct WarpRing {
   const cd* bkw;        // full spectral key in global memory
-  cd* ring;             // K1B_SLOTS stages in shared memory
-  uint64_t* full;       // [slots] completes when a stage's bytes have landed
-  uint32_t* released;   // [slots] warps that are done with the stage in the slot
-  int stage;            // next stage this warp will consume (2*i + p)
-  int n_stages;
+  cd* ring;             // WR_SLOTS chunks in shared memory
+  uint64_t* full;       // [slots] completes when a chunk's bytes have landed
+  uint32_t* released;   // [slots] warps that are done with the chunk in the slot
+  uint32_t full_u32;    // shared-space address of full[0]
+  int chunk;            // next chunk this warp will consume (4*i + 2*p + lvl)
+  int n_chunks;
 
-  static __device__ __forceinline__ int slot(int s) { return s % K1B_SLOTS; }
-  static __device__ __forceinline__ uint32_t parity(int s) { return (uint32_t)(s / K1B_SLOTS) & 1u; }
+  static __device__ __forceinline__ int slot(int s) { return s % WR_SLOTS; }
+  static __device__ __forceinline__ uint32_t parity(int s) { return (uint32_t)(s / WR_SLOTS) & 1u; }
   __device__ __forceinline__ void issue(int s) {
-    mbar_expect_tx(&full[slot(s)], STAGE_BYTES);
-    bulk_load(ring + (size_t)slot(s) * STAGE_CD, bkw + (size_t)s * STAGE_CD, STAGE_BYTES, &full[slot(s)]);
+    mbar_expect_tx(&full[slot(s)], WR_CHUNK_BYTES);
+    bulk_load(ring + (size_t)slot(s) * WCHUNK_CD, bkw + (size_t)s * WCHUNK_CD, WR_CHUNK_BYTES, &full[slot(s)]);
   }
-  __device__ __forceinline__ const cd* acquire(int, int) {
-    mbar_wait(&full[slot(stage)], parity(stage));
-    return ring + (size_t)slot(stage) * STAGE_CD;
+#ifdef TFB_K1D_PROBE
+  long long waited = 0, polls = 0;
+#endif
+  __device__ __forceinline__ const cd* acquire_chunk(int, int, int) {
+#ifdef TFB_K1D_PROBE
+    const long long t0 = clock64();
+    while (!mbar_test_u32(full_u32 + 8u * (uint32_t)slot(chunk), parity(chunk))) {
+      __nanosleep(100);
+      ++polls;
+    }
+    waited += clock64() - t0;
+#else
+    mbar_wait_u32(full_u32 + 8u * (uint32_t)slot(chunk), parity(chunk));
+#endif
+    return ring + (size_t)slot(chunk) * WCHUNK_CD;
   }
   __device__ __forceinline__ cd load(const cd* q) const { return *q; }
   __device__ __forceinline__ void release() {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
-      const int sl = slot(stage);
+      const int sl = slot(chunk);
       if (atomicAdd(&released[sl], 1u) == (uint32_t)(K1D_WARPS - 1)) {  // last one out refills the slot
         released[sl] = 0;
         __threadfence_block();
-        if (stage + K1B_SLOTS < n_stages) issue(stage + K1B_SLOTS);
+        if (chunk + WR_SLOTS < n_chunks) issue(chunk + WR_SLOTS);
       }
     }
-    ++stage;
+    ++chunk;
   }
   __device__ __forceinline__ void skip(int) {
-    acquire(0, 0);
-    release();
-    acquire(0, 1);
-    release();
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {
+      acquire_chunk(0, 0, 0);
+      release();
+    }
   }
 };
 
@@ -468,7 +507,39 @@ struct TmemWPark {
       r[4 * j + 3] = (uint32_t)__double2hiint(o[j].im);
     }
   }
+#ifndef TFB_K1D_ST4
+#define TFB_K1D_ST4 0  // stores only, one complex value per instruction
+#endif
+#ifndef TFB_K1D_X4
+#define TFB_K1D_X4 0  // 1: move accumulators one complex value (4 columns) per instruction (a 4-register tuple is
+                      // a natural aligned quad; 16-register tuples cost a MOV per word) -- measured slower: 83.8 vs 73.2 ms
+#endif
+  static __device__ __forceinline__ void ld4(uint32_t addr, cd& v) {
+    uint32_t r0, r1, r2, r3;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr)
+                 : "memory");
+    v = cd{__hiloint2double((int)r1, (int)r0), __hiloint2double((int)r3, (int)r2)};
+  }
+  static __device__ __forceinline__ void st4(uint32_t addr, const cd& v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+                 "r"((uint32_t)__double2loint(v.re)), "r"((uint32_t)__double2hiint(v.re)),
+                 "r"((uint32_t)__double2loint(v.im)), "r"((uint32_t)__double2hiint(v.im))
+                 : "memory");
+  }
+  // the wait makes the loaded registers valid; tying them to it keeps their uses behind it
+  static __device__ __forceinline__ void wait_ld4(cd* o) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+d"(o[0].re), "+d"(o[0].im), "+d"(o[1].re), "+d"(o[1].im), "+d"(o[2].re), "+d"(o[2].im),
+                   "+d"(o[3].re), "+d"(o[3].im)::"memory");
+  }
   __device__ __forceinline__ void load_one(int c, int qb, cd* o) const {
+#if TFB_K1D_X4
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j) ld4(taddr + 64 * c + 4 * (qb + j), o[j]);
+    wait_ld4(o);
+#else
     uint32_t r[16];
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -478,8 +549,18 @@ struct TmemWPark {
         : "r"(taddr + 64 * c + 4 * qb)
         : "memory");
     unpack(r, o);
+#endif
   }
   __device__ __forceinline__ void load(int qb, cd* o0, cd* o1) const {
+#if TFB_K1D_X4
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j) {
+      ld4(taddr + 4 * (qb + j), o0[j]);
+      ld4(taddr + 64 + 4 * (qb + j), o1[j]);
+    }
+    wait_ld4(o0);
+    wait_ld4(o1);
+#else
     uint32_t r[32];
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -494,8 +575,13 @@ struct TmemWPark {
         : "memory");
     unpack(r, o0);
     unpack(r + 16, o1);
+#endif
   }
   __device__ __forceinline__ void store_one(int c, int qb, const cd* o) const {
+#if TFB_K1D_X4 || TFB_K1D_ST4
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j) st4(taddr + 64 * c + 4 * (qb + j), o[j]);
+#else
     uint32_t r[16];
     pack(o, r);
     asm volatile(
@@ -504,6 +590,7 @@ struct TmemWPark {
         "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
         "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
+#endif
   }
   __device__ __forceinline__ void store(int qb, const cd* o0, const cd* o1) const {
     store_one(0, qb, o0);
@@ -585,7 +672,7 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
   extern __shared__ __align__(128) unsigned char smem[];
   WarpTwiddles* tw = reinterpret_cast<WarpTwiddles*>(smem);
   cd* ring = reinterpret_cast<cd*>(smem + sizeof(WarpTwiddles));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sizeof(WarpTwiddles) + K1B_SLOTS * STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sizeof(WarpTwiddles) + 4 * 16384);
   const int wid = threadIdx.x / WARP_T, t = threadIdx.x % WARP_T;
   unsigned char* mine = smem + K1D_HEADER + (size_t)wid * warp_smem(n);
   void* buf = mine;
@@ -594,9 +681,10 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
 
   for (int i = threadIdx.x; i < (int)(sizeof(WarpTwiddles) / sizeof(cd)); i += K1D_THREADS)
     reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
-  WarpRing bk{bkw, ring, bars, reinterpret_cast<uint32_t*>(bars + K1B_SLOTS), 0, 2 * n};
+  static_assert(WR_SLOTS * WR_CHUNK_BYTES <= 4 * 16384 && WR_SLOTS <= 8, "key ring does not fit its header slot");
+  WarpRing bk{bkw, ring, bars, reinterpret_cast<uint32_t*>(bars + WR_SLOTS), smem_u32(bars), 0, 4 * n};
   if (threadIdx.x == 0) {
-    for (int j = 0; j < K1B_SLOTS; ++j) {
+    for (int j = 0; j < WR_SLOTS; ++j) {
       mbar_init(&bk.full[j], 1);
       bk.released[j] = 0;
     }
@@ -618,7 +706,7 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (threadIdx.x == 0)
-    for (int j = 0; j < K1B_SLOTS; ++j) bk.issue(j);
+    for (int j = 0; j < WR_SLOTS; ++j) bk.issue(j);
   const TmemTw ttw{tmem_base + ((((uint32_t)wid & 3u) * 32u) << 16) + K1D_TMEM_TW};
   if (wid < 4) {  // one warp per lane quarter builds the twiddle table
     LaneTwiddles lt;
@@ -640,7 +728,15 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
 #else
   RegPark park;
 #endif
+#ifdef TFB_K1D_PROBE
+  const long long probe_t0 = clock64();
+#endif
   gate_bootstrap_warp(xr, yr, (int)kinds[g], n, mu, bk, ttw, acc, abar, buf, dst, t, w, park);
+#ifdef TFB_K1D_PROBE
+  if (t == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
+    printf("cta %d warp %2d: %lld cycles, %lld waiting for the key (%.1f%%), %lld polls\n", (int)blockIdx.x, wid,
+           clock64() - probe_t0, bk.waited, 100.0 * bk.waited / (double)(clock64() - probe_t0), bk.polls);
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (wid == 0)
@@ -1000,8 +1096,13 @@ static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* ki
   // K1c: up to two waves of one-gate-per-SM CTAs (four thread groups per gate) win on latency.
   // K1b keeps K1B_GROUPS gates on one SM; below one full wave of such CTAs the
   // one-gate-per-CTA kernel K1a spreads the launch over more SMs and wins.
+  // K1d (one gate per warp, twelve per SM) is the throughput kernel once a launch fills a wave of its CTAs.
   int which = ctx->force_kernel;
-  if (!which) which = k <= 2 * ctx->sm_count ? 3 : (k >= (int64_t)ctx->sm_count * K1B_GROUPS ? 2 : 1);
+  if (!which)
+    which = k <= 2 * ctx->sm_count                        ? 3
+            : k >= (int64_t)ctx->sm_count * K1D_WARPS     ? 4
+            : k >= (int64_t)ctx->sm_count * K1B_GROUPS    ? 2
+                                                          : 1;
   if (which == 4) {
     const unsigned grid = (unsigned)((k + K1D_WARPS - 1) / K1D_WARPS);
     k_gate_bootstrap_warp<<<grid, K1D_THREADS, K1D_HEADER + K1D_WARPS * warp_smem(n), st>>>(

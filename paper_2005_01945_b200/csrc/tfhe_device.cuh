@@ -395,6 +395,7 @@ TFB_HD int stage_index(int k2, int lvl, int c, int t) { return ((k2 * BK_L + lvl
 struct GlobalBk {  // plain pointer into the full key (host emulation, key setup checks)
   const cd* base;
   TFB_HD const cd* acquire(int i, int p) { return base + stage_offset(i, p); }
+  TFB_HD const cd* acquire_chunk(int i, int p, int lvl) { return base + stage_offset(i, p) + (size_t)lvl * (STAGE_CD / 2); }
   TFB_HD cd load(const cd* q) const { return *q; }
   TFB_HD void release() {}
   TFB_HD void skip(int) {}

@@ -293,7 +293,10 @@ TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
 }
 
 // Spectral key stage (i, p) in this kernel's order: [lvl][q][c][lane], prescaled by 1/512
-// (same 32 KB per stage and the same stage_offset as the 64-thread layout).
+// (same 32 KB per stage and the same stage_offset as the 64-thread layout).  The unit the
+// key ring moves is a CHUNK = one (i, p, lvl) = 16 KB: what one MAC consumes.  A key source
+// offers acquire_chunk(i, p, lvl) / load(ptr) / release() / skip(i).
+constexpr int WCHUNK_CD = WPTS * 2 * WARP_T;  // 1024 cd
 TFB_HD int wstage_index(int lvl, int q, int c, int t) { return ((lvl * WPTS + q) * 2 + c) * WARP_T + t; }
 
 // Accumulator parking.  The 2 x 16 complex accumulators of a CMux are idle while a transform
@@ -340,8 +343,8 @@ struct RegPark {  // no parking: plain registers (host emulation)
 // MAC of one forward-transformed digit polynomial x against level `lvl` of the staged key;
 // the accumulators live in the park.  FIRST starts them instead of loading them.
 template <bool FIRST, class BkSource, class Park>
-TFB_HD void wmac(Park& park, const cd* x, BkSource& bk, const cd* stage, int lvl, int t) {
-  const cd* key = stage + wstage_index(lvl, 0, 0, t);
+TFB_HD void wmac(Park& park, const cd* x, BkSource& bk, const cd* chunk, int t) {
+  const cd* key = chunk + t;
 #pragma unroll
   for (int qb = 0; qb < WPTS; qb += PARK_CH) {
     cd o0[PARK_CH], o1[PARK_CH];
@@ -381,8 +384,8 @@ TFB_HD double wdigit(uint32_t field) {
 // and decomposed from ACC for lvl 0, which also parks the level-1 digit words; taken from the
 // park for lvl 1), forward transform, MAC against the key.
 template <bool FIRST, class W, class BkSource, class Park, class Tw>
-TFB_HD void wcmux_stage(int s, const cd*& stage, const uint32_t* acc, int abar, int i, BkSource& bk, int t,
-                        const Tw& tw, void* buf, W& w, Park& park) {
+TFB_HD void wcmux_stage(int s, const uint32_t* acc, int abar, int i, BkSource& bk, int t, const Tw& tw, void* buf,
+                        W& w, Park& park) {
   const int p = s >> 1, lvl = s & 1;
   cd x[WPTS];
   uint32_t d1[WPTS];  // level-1 digit fields of (re, im), 16 bits each
@@ -391,12 +394,22 @@ TFB_HD void wcmux_stage(int s, const cd*& stage, const uint32_t* acc, int abar, 
     // compiler recomputes them here instead of carrying 64 of them across the whole CMux.
     int rot = abar;
     TFB_OPAQUE(rot);
+    // coefficient j = t + 32 mm of X^rot * P - P, mm = 0..31 (mm >= 16: the imaginary parts):
+    // the source index advances by 32 per step in the doubled index space [0, 2N), whose
+    // bit 10 is the sign of the wrapped coefficient
+    const uint32_t* poly = acc + p * RING_N;
+    const uint32_t base = (uint32_t)(t - rot);
 #pragma unroll
     for (int m = 0; m < WPTS; ++m) {
-      const uint32_t vr = rotated_diff(acc + p * RING_N, t + 32 * m, rot) + DECOMP_OFFSET;
-      const uint32_t vi = rotated_diff(acc + p * RING_N, t + 32 * m + HALF_N, rot) + DECOMP_OFFSET;
-      x[m] = cd{wdigit(digit_field(vr, 0)), wdigit(digit_field(vi, 0))};
-      d1[m] = digit_field(vr, 1) | (digit_field(vi, 1) << 16);
+      uint32_t v[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint32_t src = base + 32u * (uint32_t)(m + 16 * e);
+        const uint32_t sg = (uint32_t)((int32_t)(src << 21) >> 31);  // all ones when the wrap flips the sign
+        v[e] = ((poly[src & (RING_N - 1)] ^ sg) - sg) - poly[t + 32 * (m + 16 * e)] + DECOMP_OFFSET;
+      }
+      x[m] = cd{wdigit(v[0] >> 22), wdigit(v[1] >> 22)};
+      d1[m] = ((v[0] >> 12) & 0x3ffu) | ((v[1] << 4) & 0x3ff0000u);
     }
     park.store_digits(d1);
   } else {
@@ -405,9 +418,9 @@ TFB_HD void wcmux_stage(int s, const cd*& stage, const uint32_t* acc, int abar, 
     for (int m = 0; m < WPTS; ++m) x[m] = cd{wdigit(d1[m] & 0xffffu), wdigit(d1[m] >> 16)};
   }
   wfft_forward(x, t, tw, buf, w);
-  if (lvl == 0) stage = bk.acquire(i, p);
-  wmac<FIRST>(park, x, bk, stage, lvl, t);
-  if (lvl == 1) bk.release();
+  const cd* chunk = bk.acquire_chunk(i, p, lvl);
+  wmac<FIRST>(park, x, bk, chunk, t);
+  bk.release();
 }
 
 // One CMux step by one warp.  acc: 2 polynomials of N words in shared memory.
@@ -416,10 +429,9 @@ TFB_HD void wcmux_stage(int s, const cd*& stage, const uint32_t* acc, int abar, 
 template <class W, class BkSource, class Park, class Tw>
 TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, const Tw& tw, void* buf, W& w,
                        Park& park) {
-  const cd* stage = nullptr;
-  wcmux_stage<true>(0, stage, acc, abar, i, bk, t, tw, buf, w, park);
+  wcmux_stage<true>(0, acc, abar, i, bk, t, tw, buf, w, park);
   TFB_K1D_LOOP
-  for (int s = 1; s < 4; ++s) wcmux_stage<false>(s, stage, acc, abar, i, bk, t, tw, buf, w, park);
+  for (int s = 1; s < 4; ++s) wcmux_stage<false>(s, acc, abar, i, bk, t, tw, buf, w, park);
   TFB_K1D_LOOP
   for (int c = 0; c < 2; ++c) {
     cd x[WPTS];

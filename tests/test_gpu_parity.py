@@ -121,16 +121,17 @@ def test_edge_inputs_trivial_and_aliased(gpu, key, eval_keys):
 
 
 def test_every_kernel_variant_is_bit_exact(key, eval_keys, monkeypatch):
-    """K1a (one gate per 64-thread CTA), K1b (six gates per CTA, TMA-staged key ring), K1c (one gate
-    over four thread groups) and both key-switch modes (direct / split with atomics) on the same jobs,
-    with a gate count that leaves a ragged last CTA."""
+    """K1a (one gate per 64-thread CTA), K1b (four gates per CTA, TMA-staged key ring), K1c (one gate
+    over four thread groups), K1d (one gate per warp, twelve per CTA, tensor-memory parking) and both
+    key-switch modes (direct / split with atomics) on the same jobs, with a gate count that leaves a
+    ragged last CTA."""
     import torch
 
     from paper_2005_01945_b200 import _cabi
 
     xs, ys, kinds, bits = make_inputs(key, 45, seed=36, kinds=(np.arange(45) % 9).astype(np.uint8))
     want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
-    for variant in ("1", "2", "3"):
+    for variant in ("1", "2", "3", "4"):
         monkeypatch.setenv("TFB_FORCE_KERNEL", variant)
         ctx = _cabi.Context(0, key.params.m, key.params.mu.word, eval_keys.ring)
         ctx.call("tfb_load_keys", eval_keys.bk.ctypes.data, eval_keys.ksk.ctypes.data, 0, None)
@@ -140,11 +141,11 @@ def test_every_kernel_variant_is_bit_exact(key, eval_keys, monkeypatch):
 
 
 def test_automatic_dispatch_sizes(gpu, key, eval_keys):
-    """Launch sizes on both sides of the K1c / K1a / K1b dispatch thresholds (2 x SMs, 6 x SMs)."""
+    """Launch sizes on both sides of the K1c / K1a / K1b / K1d dispatch thresholds (2, 4, 12 x SMs)."""
     base = 64
     xs, ys, kinds, bits = make_inputs(key, base, seed=37)
     want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
-    for K in (1, 2, 297, 889, 1030):
+    for K in (1, 2, 297, 889, 1030, 1775, 1777, 1800):
         idx = np.arange(K) % base
         got = run_launch(gpu, key, xs[idx], ys[idx], kinds[idx])
         assert np.array_equal(got, want[idx]), K
