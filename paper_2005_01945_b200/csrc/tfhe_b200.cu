@@ -1090,19 +1090,26 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
   return TFB_OK;
 }
 
-static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds, const int32_t* xr,
-                               const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
+// Cost model of the four K1 variants (ms per launch on a 148-SM B200 at n = 500, measured with
+// tools/k1_ab.py; only the ratios matter).  Every variant runs in waves of one CTA set per SM:
+//   K1c 1 gate / SM, 1.41 ms per wave        K1a up to 4 gates / SM, 2.49 .. 3.74 ms per wave
+//   K1b 4 gates / SM, 3.35 ms per wave       K1d 12 gates / SM, 9.3 ms per wave
+static int pick_k1(int64_t k, int sms, double* cost) {
+  const double S = (double)sms;
+  const double waves_c = ceil(k / S), waves_b = ceil(k / (4 * S)), waves_d = ceil(k / (12 * S));
+  const double t[5] = {0.0,
+                       k <= S ? 2.49 : (k <= 2 * S ? 2.69 : (k <= 3 * S ? 3.53 : 3.74 * waves_b)),
+                       3.35 * waves_b, 1.41 * waves_c, 9.3 * waves_d};
+  int best = 3;
+  for (int w = 1; w <= 4; ++w)
+    if (t[w] < t[best]) best = w;
+  if (cost) *cost = t[best];
+  return best;
+}
+
+static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, const uint8_t* kinds, const int32_t* xr,
+                             const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
   const int n = ctx->p.n;
-  // K1c: up to two waves of one-gate-per-SM CTAs (four thread groups per gate) win on latency.
-  // K1b keeps K1B_GROUPS gates on one SM; below one full wave of such CTAs the
-  // one-gate-per-CTA kernel K1a spreads the launch over more SMs and wins.
-  // K1d (one gate per warp, twelve per SM) is the throughput kernel once a launch fills a wave of its CTAs.
-  int which = ctx->force_kernel;
-  if (!which)
-    which = k <= 2 * ctx->sm_count                        ? 3
-            : k >= (int64_t)ctx->sm_count * K1D_WARPS     ? 4
-            : k >= (int64_t)ctx->sm_count * K1B_GROUPS    ? 2
-                                                          : 1;
   if (which == 4) {
     const unsigned grid = (unsigned)((k + K1D_WARPS - 1) / K1D_WARPS);
     k_gate_bootstrap_warp<<<grid, K1D_THREADS, K1D_HEADER + K1D_WARPS * warp_smem(n), st>>>(
@@ -1121,6 +1128,25 @@ static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* ki
   ctx->launches += 1;
   TFB_CUDA(ctx, cudaGetLastError());
   return TFB_OK;
+}
+
+// K1 dispatch.  K1c (one gate over four thread groups) wins on latency, K1d (one gate per warp,
+// twelve per SM) on throughput, K1b / K1a in between.  A large launch runs its full K1d waves
+// first and hands the ragged rest to whichever variant finishes it soonest.
+static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds, const int32_t* xr,
+                               const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
+  if (ctx->force_kernel) return launch_k1_variant(ctx, ctx->force_kernel, pool, kinds, xr, yr, ext, k, st);
+  const int64_t wave_d = (int64_t)ctx->sm_count * K1D_WARPS;
+  const int64_t body = k / wave_d * wave_d, rest = k - body;
+  double whole = 0, tail = 0;
+  const int w_whole = pick_k1(k, ctx->sm_count, &whole);
+  if (body == 0 || rest == 0) return launch_k1_variant(ctx, w_whole, pool, kinds, xr, yr, ext, k, st);
+  const int w_tail = pick_k1(rest, ctx->sm_count, &tail);
+  if (9.3 * (double)(body / wave_d) + tail >= whole)
+    return launch_k1_variant(ctx, w_whole, pool, kinds, xr, yr, ext, k, st);
+  int rc = launch_k1_variant(ctx, 4, pool, kinds, xr, yr, ext, body, st);
+  if (rc) return rc;
+  return launch_k1_variant(ctx, w_tail, pool, kinds + body, xr + body, yr + body, ext + body * EXT_STRIDE, rest, st);
 }
 
 static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, const int32_t* out_rows,

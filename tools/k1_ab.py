@@ -7,7 +7,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 ap = argparse.ArgumentParser()
-ap.add_argument("--k", type=int, default=16384)
+ap.add_argument("--k", default="16384", help="comma-separated launch sizes")
 ap.add_argument("--kernels", default="2,4")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--lib", default=None)
@@ -38,9 +38,8 @@ xs = np.stack([pack(encrypt_bit(key, (g >> 1) & 1, rng)) for g in range(K)])
 ys = np.stack([pack(encrypt_bit(key, g & 1, rng)) for g in range(K)])
 kinds = np.array([(g // 4) % 8 for g in range(K)], dtype=np.uint8)
 _, want_ext = orc.gate_bootstrap_batch(xs, ys, kinds, p.mu.word, ek.bk, ek.ksk, want_ext=True)
-k = args.k
 res = {}
-for which in args.kernels.split(","):
+for which, k in [(w, int(kk)) for kk in args.k.split(",") for w in args.kernels.split(",")]:
     os.environ["TFB_FORCE_KERNEL"] = which
     ctx = _cabi.Context(0, n, p.mu.word, ek.ring)
     ctx.call("tfb_load_keys", ek.bk.ctypes.data, ek.ksk.ctypes.data, 0, None)
@@ -68,8 +67,8 @@ for which in args.kernels.split(","):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.reps
-    res[which] = {"ms": ms, "gates_per_s": k / ms * 1e3, "mismatch_words": bad}
-    print(which, res[which], flush=True)
+    res[f"{which}@{k}"] = {"ms": ms, "gates_per_s": k / ms * 1e3, "mismatch_words": bad}
+    print(which, k, res[f"{which}@{k}"], flush=True)
     ctx.close()
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 with open(os.path.join(ROOT, "gpurun_out", "k1_ab.json"), "w") as f:
