@@ -137,7 +137,7 @@ __host__ __device__ constexpr int group_smem(int n) { return GROUP_SMEM_FIXED + 
 
 __global__ void __launch_bounds__(FFT_THREADS, TFB_K1_MIN_BLOCKS) k_gate_bootstrap(
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
-    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
+    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
     const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext) {
   extern __shared__ __align__(128) unsigned char smem[];
   Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(FFT_THREADS, TFB_K1_MIN_BLOCKS) k_gate_bootstr
   for (int i = threadIdx.x; i < (int)(sizeof(Twiddles) / sizeof(cd)); i += FFT_THREADS)
     reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
   const int64_t g = blockIdx.x;
-  const uint32_t* xr = pool + (int64_t)x_rows[g] * ROW_STRIDE;
-  const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
+  const uint32_t* xr = pool + (int64_t)x_rows[g] * stride;
+  const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
   BlockSync sync;
   LdgBk bk{bkf};
   NoPark park;
@@ -177,7 +177,7 @@ struct LdgLoad {
 
 __global__ void __launch_bounds__(K1C_THREADS, 1) k_gate_bootstrap_wide(
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
-    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
+    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
     const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext) {
   extern __shared__ __align__(128) unsigned char smem[];
   Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
@@ -188,8 +188,8 @@ __global__ void __launch_bounds__(K1C_THREADS, 1) k_gate_bootstrap_wide(
   for (int i = threadIdx.x; i < (int)(sizeof(Twiddles) / sizeof(cd)); i += K1C_THREADS)
     reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
   const int64_t g = blockIdx.x;
-  const uint32_t* xr = pool + (int64_t)x_rows[g] * ROW_STRIDE;
-  const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
+  const uint32_t* xr = pool + (int64_t)x_rows[g] * stride;
+  const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
   GroupSync gsync{(int)(threadIdx.x / FFT_THREADS) + 1};
   BlockSync csync;
   gate_bootstrap_wide(xr, yr, (int)kinds[g], n, mu, bkf, tw, acc, abar, xbuf, red, ext + g * EXT_STRIDE,
@@ -314,7 +314,7 @@ struct RingBk {
 
 __global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
-    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
+    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
     const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext,
     int64_t k) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
   // tail CTA: surplus groups redo the last ciphertext (keeps the ring protocol uniform) but do not store
   const int64_t want = (int64_t)blockIdx.x * K1B_GROUPS + grp;
   const int64_t g = want < k ? want : k - 1;
-  const uint32_t* xr = pool + (int64_t)x_rows[g] * ROW_STRIDE;
-  const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
+  const uint32_t* xr = pool + (int64_t)x_rows[g] * stride;
+  const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
   uint32_t* dst = want < k ? ext + g * EXT_STRIDE : reinterpret_cast<uint32_t*>(s0);  // scratch sink
   GroupSync sync{grp + 1};
 #if TFB_K1B_TMEM
@@ -666,7 +666,7 @@ struct TmemTw {
 
 __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
-    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int n, uint32_t mu,
+    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
     const cd* __restrict__ bkw, const WarpTwiddles* __restrict__ tw_global, uint32_t* __restrict__ ext,
     int64_t k) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -719,8 +719,8 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
   // tail CTA: surplus warps redo the last ciphertext (keeps the ring protocol uniform) but do not store
   const int64_t want = (int64_t)blockIdx.x * K1D_WARPS + wid;
   const int64_t g = want < k ? want : k - 1;
-  const uint32_t* xr = pool + (int64_t)x_rows[g] * ROW_STRIDE;
-  const uint32_t* yr = pool + (int64_t)y_rows[g] * ROW_STRIDE;
+  const uint32_t* xr = pool + (int64_t)x_rows[g] * stride;
+  const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
   uint32_t* dst = want < k ? ext + g * EXT_STRIDE : nullptr;  // null: no extract
   DevWarp w;
 #if TFB_K1D_TMEM
@@ -755,8 +755,8 @@ constexpr int KS_CHUNK_R = KS_CHUNK_I * KS_T;
 __global__ void __launch_bounds__(KS_THREADS) k_key_switch(const uint32_t* __restrict__ ext,
                                                            const int32_t* __restrict__ ksk,
                                                            uint32_t* __restrict__ pool,
-                                                           const int32_t* __restrict__ out_rows, int n,
-                                                           int64_t k, int i_per_cta) {
+                                                           const int32_t* __restrict__ out_rows, int stride,
+                                                           int n, int64_t k, int i_per_cta) {
   // gridDim.y > 1: the ring coefficients are split over blockIdx.y and the partial sums are
   // combined with integer atomics into rows zeroed by k_rows_zero (small launches: latency).
   __shared__ __align__(16) int32_t digits[KS_CHUNK_R][KS_CT];
@@ -805,23 +805,23 @@ __global__ void __launch_bounds__(KS_THREADS) k_key_switch(const uint32_t* __res
 #pragma unroll
   for (int c = 0; c < KS_CT; ++c) {
     if (c0 + c >= k) break;
-    uint32_t* row = pool + (int64_t)out_rows[c0 + c] * ROW_STRIDE;
+    uint32_t* row = pool + (int64_t)out_rows[c0 + c] * stride;  // only columns 0..n are written: rows may be packed
     const uint32_t body = (blockIdx.y == 0) ? ext[(c0 + c) * EXT_STRIDE + RING_N] : 0u;
     const uint32_t v0 = (tid == n ? body : 0u) - (uint32_t)acc0[c];
     const uint32_t v1 = (tid + KS_THREADS == n ? body : 0u) - (uint32_t)acc1[c];
     if (split) {
-      atomicAdd(row + tid, v0);
-      atomicAdd(row + tid + KS_THREADS, v1);
+      if (tid <= n) atomicAdd(row + tid, v0);
+      if (tid + KS_THREADS <= n) atomicAdd(row + tid + KS_THREADS, v1);
     } else {
-      row[tid] = v0;
-      row[tid + KS_THREADS] = v1;
+      if (tid <= n) row[tid] = v0;
+      if (tid + KS_THREADS <= n) row[tid + KS_THREADS] = v1;
     }
   }
 }
 
-__global__ void k_rows_zero(uint32_t* __restrict__ pool, const int32_t* __restrict__ rows) {
-  uint32_t* dst = pool + (int64_t)rows[blockIdx.x] * ROW_STRIDE;
-  for (int c = threadIdx.x; c < ROW_STRIDE; c += blockDim.x) dst[c] = 0u;
+__global__ void k_rows_zero(uint32_t* __restrict__ pool, const int32_t* __restrict__ rows, int stride, int n) {
+  uint32_t* dst = pool + (int64_t)rows[blockIdx.x] * stride;
+  for (int c = threadIdx.x; c <= n; c += blockDim.x) dst[c] = 0u;
 }
 
 // ------------------------------------------------------------------------------------
@@ -1107,23 +1107,23 @@ static int pick_k1(int64_t k, int sms, double* cost) {
   return best;
 }
 
-static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, const uint8_t* kinds, const int32_t* xr,
-                             const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
+static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, int stride, const uint8_t* kinds,
+                             const int32_t* xr, const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
   const int n = ctx->p.n;
   if (which == 4) {
     const unsigned grid = (unsigned)((k + K1D_WARPS - 1) / K1D_WARPS);
     k_gate_bootstrap_warp<<<grid, K1D_THREADS, K1D_HEADER + K1D_WARPS * warp_smem(n), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ext, k);
+        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ext, k);
   } else if (which == 3) {
     k_gate_bootstrap_wide<<<(unsigned)k, K1C_THREADS, k1c_smem(n), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
+        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
   } else if (which == 2) {
     const unsigned grid = (unsigned)((k + K1B_GROUPS - 1) / K1B_GROUPS);
     k_gate_bootstrap_ring<<<grid, K1B_THREADS, K1B_HEADER + K1B_GROUPS * group_smem(n), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext, k);
+        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext, k);
   } else {
     k_gate_bootstrap<<<(unsigned)k, FFT_THREADS, (int)sizeof(Twiddles) + group_smem(n), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
+        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
   }
   ctx->launches += 1;
   TFB_CUDA(ctx, cudaGetLastError());
@@ -1133,33 +1133,35 @@ static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, const ui
 // K1 dispatch.  K1c (one gate over four thread groups) wins on latency, K1d (one gate per warp,
 // twelve per SM) on throughput, K1b / K1a in between.  A large launch runs its full K1d waves
 // first and hands the ragged rest to whichever variant finishes it soonest.
-static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds, const int32_t* xr,
+static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, int stride, const uint8_t* kinds, const int32_t* xr,
                                const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
-  if (ctx->force_kernel) return launch_k1_variant(ctx, ctx->force_kernel, pool, kinds, xr, yr, ext, k, st);
+  if (ctx->force_kernel)
+    return launch_k1_variant(ctx, ctx->force_kernel, pool, stride, kinds, xr, yr, ext, k, st);
   const int64_t wave_d = (int64_t)ctx->sm_count * K1D_WARPS;
   const int64_t body = k / wave_d * wave_d, rest = k - body;
   double whole = 0, tail = 0;
   const int w_whole = pick_k1(k, ctx->sm_count, &whole);
-  if (body == 0 || rest == 0) return launch_k1_variant(ctx, w_whole, pool, kinds, xr, yr, ext, k, st);
+  if (body == 0 || rest == 0) return launch_k1_variant(ctx, w_whole, pool, stride, kinds, xr, yr, ext, k, st);
   const int w_tail = pick_k1(rest, ctx->sm_count, &tail);
   if (9.3 * (double)(body / wave_d) + tail >= whole)
-    return launch_k1_variant(ctx, w_whole, pool, kinds, xr, yr, ext, k, st);
-  int rc = launch_k1_variant(ctx, 4, pool, kinds, xr, yr, ext, body, st);
+    return launch_k1_variant(ctx, w_whole, pool, stride, kinds, xr, yr, ext, k, st);
+  int rc = launch_k1_variant(ctx, 4, pool, stride, kinds, xr, yr, ext, body, st);
   if (rc) return rc;
-  return launch_k1_variant(ctx, w_tail, pool, kinds + body, xr + body, yr + body, ext + body * EXT_STRIDE, rest, st);
+  return launch_k1_variant(ctx, w_tail, pool, stride, kinds + body, xr + body, yr + body, ext + body * EXT_STRIDE,
+                           rest, st);
 }
 
-static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, const int32_t* out_rows,
+static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, int stride, const int32_t* out_rows,
                              int64_t k, cudaStream_t st) {
   const unsigned tiles = (unsigned)((k + KS_CT - 1) / KS_CT);
   // small launches: split the 1024 ring coefficients over up to 64 CTAs per tile to fill the chip
   unsigned split = 1;
   while (split < RING_N / KS_CHUNK_I && tiles * split < 2u * (unsigned)ctx->sm_count) split *= 2;
   if (split > 1) {
-    k_rows_zero<<<(unsigned)k, 128, 0, st>>>((uint32_t*)pool, out_rows);
+    k_rows_zero<<<(unsigned)k, 128, 0, st>>>((uint32_t*)pool, out_rows, stride, ctx->p.n);
     ctx->launches += 1;
   }
-  k_key_switch<<<dim3(tiles, split), KS_THREADS, 0, st>>>(ext, ctx->d_ksk, (uint32_t*)pool, out_rows, ctx->p.n, k,
+  k_key_switch<<<dim3(tiles, split), KS_THREADS, 0, st>>>(ext, ctx->d_ksk, (uint32_t*)pool, out_rows, stride, ctx->p.n, k,
                                                          RING_N / (int)split);
   ctx->launches += 1;
   TFB_CUDA(ctx, cudaGetLastError());
@@ -1187,8 +1189,8 @@ int tfb_gate_launch(tfb_ctx* ctx, void* pool, const uint8_t* kinds, const int32_
   cudaStream_t st = (cudaStream_t)stream;
   TFB_CUDA(ctx, cudaSetDevice(ctx->device));
   if ((rc = ensure_ext(ctx, k))) return rc;
-  if ((rc = launch_blind_rotate(ctx, pool, kinds, xr, yr, ctx->d_ext, k, st))) return rc;
-  return launch_key_switch(ctx, ctx->d_ext, pool, out_rows, k, st);
+  if ((rc = launch_blind_rotate(ctx, pool, ROW_STRIDE, kinds, xr, yr, ctx->d_ext, k, st))) return rc;
+  return launch_key_switch(ctx, ctx->d_ext, pool, ROW_STRIDE, out_rows, k, st);
 }
 
 int tfb_debug_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds, const int32_t* xr,
@@ -1197,7 +1199,7 @@ int tfb_debug_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds,
   if (rc) return rc;
   if (!pool || !kinds || !xr || !yr || !ext) return TFB_ERR_INVALID;
   TFB_CUDA(ctx, cudaSetDevice(ctx->device));
-  return launch_blind_rotate(ctx, pool, kinds, xr, yr, ext, k, (cudaStream_t)stream);
+  return launch_blind_rotate(ctx, pool, ROW_STRIDE, kinds, xr, yr, ext, k, (cudaStream_t)stream);
 }
 
 int tfb_debug_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, const int32_t* out_rows, int64_t k,
@@ -1206,7 +1208,7 @@ int tfb_debug_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, const in
   if (rc) return rc;
   if (!pool || !ext || !out_rows) return TFB_ERR_INVALID;
   TFB_CUDA(ctx, cudaSetDevice(ctx->device));
-  return launch_key_switch(ctx, ext, pool, out_rows, k, (cudaStream_t)stream);
+  return launch_key_switch(ctx, ext, pool, ROW_STRIDE, out_rows, k, (cudaStream_t)stream);
 }
 
 int tfb_gate_launch_host(tfb_ctx* ctx, const uint32_t* x, const uint32_t* y, const uint8_t* kinds,
@@ -1225,7 +1227,7 @@ int tfb_gate_launch_host(tfb_ctx* ctx, const uint32_t* x, const uint32_t* y, con
     ctx->host_cap = 0;
     int64_t cap = 256;
     while (cap < k) cap *= 2;
-    TFB_CUDA(ctx, cudaMalloc(&ctx->d_hx, (size_t)3 * cap * ROW_STRIDE * 4));
+    TFB_CUDA(ctx, cudaMalloc(&ctx->d_hx, (size_t)3 * cap * (ctx->p.n + 1) * 4));  // packed rows, as on the host
     TFB_CUDA(ctx, cudaMalloc(&ctx->d_hkinds, (size_t)cap));
     TFB_CUDA(ctx, cudaMalloc(&ctx->d_hrows, (size_t)3 * cap * 4));
     k_identity_rows<<<(unsigned)((3 * cap + 255) / 256), 256>>>(ctx->d_hrows, 3 * cap, 0);
@@ -1235,10 +1237,10 @@ int tfb_gate_launch_host(tfb_ctx* ctx, const uint32_t* x, const uint32_t* y, con
     ctx->host_cap = cap;
   }
   const int64_t cap = ctx->host_cap;
-  const size_t wpitch = (size_t)(ctx->p.n + 1) * 4, dpitch = (size_t)ROW_STRIDE * 4;
+  const int stride = ctx->p.n + 1;  // the staging rows are packed like the host rows: plain 1-D copies
   uint32_t* dx = ctx->d_hx;
-  uint32_t* dy = ctx->d_hx + (size_t)cap * ROW_STRIDE;
-  uint32_t* dout = ctx->d_hx + (size_t)2 * cap * ROW_STRIDE;
+  uint32_t* dy = ctx->d_hx + (size_t)cap * stride;
+  uint32_t* dout = ctx->d_hx + (size_t)2 * cap * stride;
   if ((rc = ensure_ext(ctx, k))) return rc;
   if (!ctx->s_in) {
     TFB_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
@@ -1250,27 +1252,27 @@ int tfb_gate_launch_host(tfb_ctx* ctx, const uint32_t* x, const uint32_t* y, con
   // Three-stage pipeline over chunks of the launch: host->device copy of chunk c+1 and
   // device->host copy of chunk c-1 overlap the kernels of chunk c (rows: x = [0,cap),
   // y = [cap,2cap), out = [2cap,3cap) of the d_hx pool; chunks use disjoint row ranges).
-  const int64_t chunk = k >= 4 * HOST_CHUNK ? HOST_CHUNK : k;
+  // The first chunk is short (two K1d waves) so that the kernels start after a small copy.
+  const int64_t first = 2 * (int64_t)ctx->sm_count * K1D_WARPS;
   int slot = 0;
-  for (int64_t c0 = 0; c0 < k; c0 += chunk, slot = (slot + 1) % HOST_EVENTS) {
-    const int64_t kc = (k - c0 < chunk) ? k - c0 : chunk;
-    const size_t doff = (size_t)c0 * ROW_STRIDE, hoff = (size_t)c0 * (ctx->p.n + 1);
-    TFB_CUDA(ctx, cudaMemcpy2DAsync(dx + doff, dpitch, x + hoff, wpitch, wpitch, (size_t)kc, cudaMemcpyHostToDevice,
-                                    ctx->s_in));
-    TFB_CUDA(ctx, cudaMemcpy2DAsync(dy + doff, dpitch, y + hoff, wpitch, wpitch, (size_t)kc, cudaMemcpyHostToDevice,
-                                    ctx->s_in));
+  for (int64_t c0 = 0; c0 < k; slot = (slot + 1) % HOST_EVENTS) {
+    int64_t kc = (c0 == 0 && k > 2 * first) ? first : HOST_CHUNK;
+    if (k - c0 < kc + first / 2) kc = k - c0;  // no crumbs: the last chunk absorbs a short rest
+    const size_t off = (size_t)c0 * stride, bytes = (size_t)kc * stride * 4;
+    TFB_CUDA(ctx, cudaMemcpyAsync(dx + off, x + off, bytes, cudaMemcpyHostToDevice, ctx->s_in));
+    TFB_CUDA(ctx, cudaMemcpyAsync(dy + off, y + off, bytes, cudaMemcpyHostToDevice, ctx->s_in));
     TFB_CUDA(ctx, cudaMemcpyAsync(ctx->d_hkinds + c0, kinds + c0, (size_t)kc, cudaMemcpyHostToDevice, ctx->s_in));
     TFB_CUDA(ctx, cudaEventRecord(ctx->ev_in[slot], ctx->s_in));
     TFB_CUDA(ctx, cudaStreamWaitEvent(ctx->s_run, ctx->ev_in[slot], 0));
     uint32_t* ext = ctx->d_ext + (size_t)c0 * EXT_STRIDE;
-    if ((rc = launch_blind_rotate(ctx, ctx->d_hx, ctx->d_hkinds + c0, ctx->d_hrows + c0, ctx->d_hrows + cap + c0, ext,
-                                  kc, ctx->s_run)))
+    if ((rc = launch_blind_rotate(ctx, ctx->d_hx, stride, ctx->d_hkinds + c0, ctx->d_hrows + c0,
+                                  ctx->d_hrows + cap + c0, ext, kc, ctx->s_run)))
       return rc;
-    if ((rc = launch_key_switch(ctx, ext, ctx->d_hx, ctx->d_hrows + 2 * cap + c0, kc, ctx->s_run))) return rc;
+    if ((rc = launch_key_switch(ctx, ext, ctx->d_hx, stride, ctx->d_hrows + 2 * cap + c0, kc, ctx->s_run))) return rc;
     TFB_CUDA(ctx, cudaEventRecord(ctx->ev_run[slot], ctx->s_run));
     TFB_CUDA(ctx, cudaStreamWaitEvent(ctx->s_out, ctx->ev_run[slot], 0));
-    TFB_CUDA(ctx, cudaMemcpy2DAsync(out + hoff, wpitch, dout + doff, dpitch, wpitch, (size_t)kc,
-                                    cudaMemcpyDeviceToHost, ctx->s_out));
+    TFB_CUDA(ctx, cudaMemcpyAsync(out + off, dout + off, bytes, cudaMemcpyDeviceToHost, ctx->s_out));
+    c0 += kc;
   }
   TFB_CUDA(ctx, cudaStreamSynchronize(ctx->s_out));
   TFB_CUDA(ctx, cudaStreamSynchronize(ctx->s_run));
