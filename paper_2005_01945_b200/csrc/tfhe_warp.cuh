@@ -234,9 +234,11 @@ TFB_HD void wflip_odd(cd* x, uint32_t sgn) {
 //   in : x[m] = c_{t+32m} = a_{t+32m} + i a_{t+32m+512}   (untwisted)
 //   out: x[q] = Z[wspectral_index(t, q)],  Z_k = sum_j c_j exp(i pi j / N) exp(2 pi i j k / 512)
 // buf: WBUF_BYTES of shared memory private to the warp.
-template <class W, class Tw>
+// FLIP = false: the caller has already applied the sign (-1)^(m h) to x[m] (the CMux folds it
+// into the integer -> double conversion, where it is free).
+template <bool FLIP = true, class W, class Tw>
 TFB_HD void wfft_forward(cd* x, int t, const Tw& tw, void* buf, W& w) {
-  wflip_odd(x, (uint32_t)(t >> 4) << 31);
+  if (FLIP) wflip_odd(x, (uint32_t)(t >> 4) << 31);
 #pragma unroll
   for (int m = 1; m < WPTS; ++m) x[m] = cmul(x[m], twist16(m));
   dft16<1>(x);
@@ -265,7 +267,8 @@ TFB_HD void wfft_forward(cd* x, int t, const Tw& tw, void* buf, W& w) {
 // stage by stage.
 //   in : x[q] = S[wspectral_index(t, q)]
 //   out: x[m] = c_{t+32m}  (re -> coefficient t+32m, im -> coefficient t+32m+512)
-template <class W, class Tw>
+// FLIP = false: the outputs are left as x[m] (-1)^(m h); the CMux folds the sign into the rounding.
+template <bool FLIP = true, class W, class Tw>
 TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
   dft16<-1>(x);
   wexchange<false>(x, t, buf, w);
@@ -289,7 +292,7 @@ TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
   dft16<-1>(x);
 #pragma unroll
   for (int m = 1; m < WPTS; ++m) x[m] = cmulc(x[m], twist16(m));
-  wflip_odd(x, (uint32_t)(t >> 4) << 31);
+  if (FLIP) wflip_odd(x, (uint32_t)(t >> 4) << 31);
 }
 
 // Spectral key stage (i, p) in this kernel's order: [lvl][q][c][lane], prescaled by 1/512
@@ -379,6 +382,14 @@ TFB_HD double wdigit(uint32_t field) {
   return digit_to_double(field);
 #endif
 }
+// sg * digit for sg = +-1 (the lane sign of the odd inputs): one FMA instead of the DADD, exact
+TFB_HD double wdigit_signed(uint32_t field, double sg, double neg_sg_bias) {
+  return fma(bits_to_double(0x4330000000000000ull | (uint64_t)field), sg, neg_sg_bias);
+}
+// round-to-nearest-even(sg * x) mod 2^32 for sg = +-1
+TFB_HD uint32_t round_to_word_signed(double x, double sg) {
+  return (uint32_t)double_to_bits(fma(x, sg, 6755399441055744.0));
+}
 
 // Stage s = 2p + lvl of a CMux: digits of accumulator polynomial p at gadget level lvl (read
 // and decomposed from ACC for lvl 0, which also parks the level-1 digit words; taken from the
@@ -389,6 +400,8 @@ TFB_HD void wcmux_stage(int s, const uint32_t* acc, int abar, int i, BkSource& b
   const int p = s >> 1, lvl = s & 1;
   cd x[WPTS];
   uint32_t d1[WPTS];  // level-1 digit fields of (re, im), 16 bits each
+  // lanes with h = 1 feed the transform -x[m] for odd m (see wfft_forward): sign folded into the conversion
+  const double sg = (t >> 4) ? -1.0 : 1.0, nsb = -sg * (4503599627370496.0 + 512.0);
   if (lvl == 0) {
     // The rotation indices depend only on (abar, lane); hidden behind an opaque copy the
     // compiler recomputes them here instead of carrying 64 of them across the whole CMux.
@@ -408,16 +421,19 @@ TFB_HD void wcmux_stage(int s, const uint32_t* acc, int abar, int i, BkSource& b
         const uint32_t sg = (uint32_t)((int32_t)(src << 21) >> 31);  // all ones when the wrap flips the sign
         v[e] = ((poly[src & (RING_N - 1)] ^ sg) - sg) - poly[t + 32 * (m + 16 * e)] + DECOMP_OFFSET;
       }
-      x[m] = cd{wdigit(v[0] >> 22), wdigit(v[1] >> 22)};
+      x[m] = (m & 1) ? cd{wdigit_signed(v[0] >> 22, sg, nsb), wdigit_signed(v[1] >> 22, sg, nsb)}
+                     : cd{wdigit(v[0] >> 22), wdigit(v[1] >> 22)};
       d1[m] = ((v[0] >> 12) & 0x3ffu) | ((v[1] << 4) & 0x3ff0000u);
     }
     park.store_digits(d1);
   } else {
     park.load_digits(d1);
 #pragma unroll
-    for (int m = 0; m < WPTS; ++m) x[m] = cd{wdigit(d1[m] & 0xffffu), wdigit(d1[m] >> 16)};
+    for (int m = 0; m < WPTS; ++m)
+      x[m] = (m & 1) ? cd{wdigit_signed(d1[m] & 0xffffu, sg, nsb), wdigit_signed(d1[m] >> 16, sg, nsb)}
+                     : cd{wdigit(d1[m] & 0xffffu), wdigit(d1[m] >> 16)};
   }
-  wfft_forward(x, t, tw, buf, w);
+  wfft_forward<false>(x, t, tw, buf, w);
   const cd* chunk = bk.acquire_chunk(i, p, lvl);
   wmac<FIRST>(park, x, bk, chunk, t);
   bk.release();
@@ -437,11 +453,12 @@ TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, cons
     cd x[WPTS];
 #pragma unroll
     for (int qb = 0; qb < WPTS; qb += PARK_CH) park.load_one(c, qb, x + qb);
-    wfft_inverse(x, t, tw, buf, w);
+    wfft_inverse<false>(x, t, tw, buf, w);
+    const double sg = (t >> 4) ? -1.0 : 1.0;  // the inverse leaves -x[m] for odd m on the lanes with h = 1
 #pragma unroll
     for (int m = 0; m < WPTS; ++m) {
-      acc[c * RING_N + t + 32 * m] += round_to_word(x[m].re);
-      acc[c * RING_N + t + 32 * m + HALF_N] += round_to_word(x[m].im);
+      acc[c * RING_N + t + 32 * m] += (m & 1) ? round_to_word_signed(x[m].re, sg) : round_to_word(x[m].re);
+      acc[c * RING_N + t + 32 * m + HALF_N] += (m & 1) ? round_to_word_signed(x[m].im, sg) : round_to_word(x[m].im);
     }
   }
   w();
