@@ -127,10 +127,12 @@ TFB_HD void dft16(cd* x) {
     }
 }
 
-// Exchange buffer slot of U[r][k1][b]; the XOR makes the accesses of both sides (fixed (k1, b)
-// over consecutive r; fixed r over consecutive k1) bank-conflict-free for 16-byte and for
-// 8-byte elements.
-TFB_HD int wslot(int r, int k1, int b) { return 32 * r + ((k1 + 16 * b) ^ (r & 15)); }
+// Exchange buffer slot of U[r][k1][b]: rows of 32 values padded to 33, so that both sides
+// (fixed (k1, b) over consecutive r; fixed r over consecutive k1) are bank-conflict-free for
+// 16-byte and for 8-byte elements AND every address is (lane part) + (compile-time register
+// part): no per-element address arithmetic, the register part rides in the instruction.
+constexpr int WX_ROW = 33;
+TFB_HD int wslot(int r, int k1, int b) { return WX_ROW * r + k1 + 16 * b; }
 
 // Spectral index held by (lane t, register q) after wfft_forward.
 TFB_HD int wspectral_index(int t, int q) { return (t & 15) + 16 * (2 * q + (t >> 4)); }
@@ -144,7 +146,7 @@ TFB_HD int wspectral_index(int t, int q) { return (t & 15) + 16 * (2 * q + (t >>
 #define TFB_K1D_SPLIT 1
 #endif
 constexpr bool WX_SPLIT = TFB_K1D_SPLIT != 0;
-constexpr int WBUF_BYTES = HALF_N * (WX_SPLIT ? 8 : 16);
+constexpr int WBUF_BYTES = WX_ROW * 16 * (WX_SPLIT ? 8 : 16);
 
 template <bool FWD>
 TFB_HD int wx_src(int t, int k) {  // slot of register k on the side that holds (r, h)-ordered data

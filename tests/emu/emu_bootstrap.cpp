@@ -207,7 +207,7 @@ extern "C" {
 void emu_w_fft_forward(const int32_t* poly, double* spec_out) {
   WarpTwiddles tw;
   fill_warp_twiddles(&tw);
-  std::vector<cd> buf(HALF_N);
+  std::vector<cd> buf(WBUF_BYTES / sizeof(cd) + 1);
   cd* out = reinterpret_cast<cd*>(spec_out);
   const uint32_t* src = reinterpret_cast<const uint32_t*>(poly);
   run_warp([&](int t, EmuWarp& w) {
@@ -224,7 +224,7 @@ void emu_w_fft_forward(const int32_t* poly, double* spec_out) {
 void emu_w_fft_inverse(const double* spec_in, uint32_t* poly_out) {
   WarpTwiddles tw;
   fill_warp_twiddles(&tw);
-  std::vector<cd> buf(HALF_N);
+  std::vector<cd> buf(WBUF_BYTES / sizeof(cd) + 1);
   const cd* in = reinterpret_cast<const cd*>(spec_in);
   run_warp([&](int t, EmuWarp& w) {
     cd x[WPTS];
@@ -247,7 +247,7 @@ void emu_w_bk_transform(const int32_t* bk_raw, int n, double* bkf_out) {
   WarpTwiddles tw;
   fill_warp_twiddles(&tw);
   cd* bkf = reinterpret_cast<cd*>(bkf_out);
-  std::vector<cd> buf(HALF_N);
+  std::vector<cd> buf(WBUF_BYTES / sizeof(cd) + 1);
   for (int64_t poly = 0; poly < (int64_t)n * BK_ROWS * 2; ++poly) {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(bk_raw) + poly * RING_N;
     const int c = (int)(poly & 1);
@@ -272,7 +272,7 @@ void emu_w_gate_bootstrap(const uint32_t* x, const uint32_t* y, const uint8_t* k
   fill_warp_twiddles(&tw);
   const cd* bkf = reinterpret_cast<const cd*>(bkf_in);
   for (int64_t g = 0; g < k; ++g) {
-    std::vector<cd> buf(HALF_N);
+    std::vector<cd> buf(WBUF_BYTES / sizeof(cd) + 1);
     std::vector<uint32_t> acc(2 * RING_N), ext(EXT_STRIDE);
     std::vector<uint16_t> abar(n + 1);
     run_warp([&](int t, EmuWarp& w) {
