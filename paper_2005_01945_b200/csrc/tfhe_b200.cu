@@ -491,8 +491,36 @@ struct DevWarp {
 // 338 B/clk/SM loads, 895 B/clk/SM stores, concurrent with the shared-memory pipe;
 // tools/microbench/tmem_shfl_bw.cu).  A warp's slice is 128 columns: polynomial c at
 // columns 64c .. 64c+63, a chunk of PARK_CH complex values is 16 columns.
+// 16 tensor-memory columns in flight: the registers are valid only after settle (tcgen05.wait::ld);
+// tying them to the wait as in/out operands keeps every use of them behind it.
+struct TmemChunk {
+  uint32_t r[16];
+};
+__device__ __forceinline__ void tmem_issue16(uint32_t addr, TmemChunk& ch) {
+  uint32_t* r = ch.r;
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_settle16(TmemChunk& ch) {
+  uint32_t* r = ch.r;
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])::"memory");
+}
+
 struct TmemWPark {
+  typedef TmemChunk Chunk;
   uint32_t taddr;  // (lane << 16) | first column of this warp's slice
+  __device__ __forceinline__ void issue_one(int c, int qb, Chunk& ch) const { tmem_issue16(taddr + 64 * c + 4 * qb, ch); }
+  __device__ __forceinline__ void settle_one(Chunk& ch, cd* o) const {
+    tmem_settle16(ch);
+    unpack(ch.r, o);
+  }
   static __device__ __forceinline__ void unpack(const uint32_t* r, cd* o) {
 #pragma unroll
     for (int j = 0; j < PARK_CH; ++j)
@@ -623,7 +651,23 @@ constexpr uint32_t K1D_TMEM_NEED = K1D_TMEM_TW + 68;                      // 16 
 // Per-lane twiddle table in tensor memory (shared by the warps of a lane quarter): 16 pass-1
 // twiddles at columns 4k .. 4k+3, the radix-2 twiddle at columns 64 .. 67.
 struct TmemTw {
+  typedef TmemChunk Chunk;
   uint32_t taddr;  // (lane << 16) | first column of the table
+  __device__ __forceinline__ void issue4(int kb, Chunk& ch) const { tmem_issue16(taddr + 4 * kb, ch); }
+  __device__ __forceinline__ void settle4(Chunk& ch, cd* w) const {
+    tmem_settle16(ch);
+    TmemWPark::unpack(ch.r, w);
+  }
+  __device__ __forceinline__ void issue_c(Chunk& ch) const {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(ch.r[0]), "=r"(ch.r[1]), "=r"(ch.r[2]), "=r"(ch.r[3])
+                 : "r"(taddr + 64)
+                 : "memory");
+  }
+  __device__ __forceinline__ cd settle_c(Chunk& ch) const {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(ch.r[0]), "+r"(ch.r[1]), "+r"(ch.r[2]), "+r"(ch.r[3])::"memory");
+    return cd{__hiloint2double((int)ch.r[1], (int)ch.r[0]), __hiloint2double((int)ch.r[3], (int)ch.r[2])};
+  }
   __device__ __forceinline__ void get4(int kb, cd* w) const {
     uint32_t r[16];
     asm volatile(

@@ -184,7 +184,7 @@ TFB_HD void wexchange(cd* x, int t, void* buf, W& w) {
 // The 16 pass-1 twiddles of a lane in register order (0..7 from sa, 8..15 from sb, each times
 // g, g^2, ...) and the radix-2 twiddle c.  Built once per lane; a twiddle provider hands them
 // to the transforms in chunks of four:
-//   get4(kb, w): twiddles kb .. kb+3;   cc(): the radix-2 twiddle
+//   issue4(kb, chunk) / settle4(chunk, w): twiddles kb .. kb+3;   issue_c / settle_c: the radix-2 twiddle
 // (the B200 kernel keeps the table in tensor memory: rebuilding the chain inside every
 // transform costs 56 FP64 instructions per transform on the pipe that limits K1d).
 struct LaneTwiddles {
@@ -203,13 +203,25 @@ TFB_HD void build_lane_twiddles(const WarpTwiddles* tw, int t, LaneTwiddles* out
   }
   out->c = tw->c[t];
 }
+// Providers split every read into issue (start the load into a Chunk) and settle (the values
+// are valid, unpack them): tensor-memory loads are asynchronous, so a transform issues the
+// next chunk before it works on the current one and the load latency hides behind FP64 work.
+struct MemChunk4 {
+  cd v[4];
+};
 struct MemTw {  // table in addressable memory (host emulation, key setup kernel)
+  typedef MemChunk4 Chunk;
   const LaneTwiddles* lt;
-  TFB_HD void get4(int kb, cd* w) const {
+  TFB_HD void issue4(int kb, Chunk& ch) const {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) w[j] = lt->w[kb + j];
+    for (int j = 0; j < 4; ++j) ch.v[j] = lt->w[kb + j];
   }
-  TFB_HD cd cc() const { return lt->c; }
+  TFB_HD void issue_c(Chunk& ch) const { ch.v[0] = lt->c; }
+  TFB_HD void settle4(Chunk& ch, cd* w) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = ch.v[j];
+  }
+  TFB_HD cd settle_c(Chunk& ch) const { return ch.v[0]; }
 };
 
 // flip the sign of x[m], odd m, on the lanes with h = 1 (sgn = h << 31): multiplying the
@@ -240,6 +252,8 @@ TFB_HD void wflip_odd(cd* x, uint32_t sgn) {
 // into the integer -> double conversion, where it is free).
 template <bool FLIP = true, class W, class Tw>
 TFB_HD void wfft_forward(cd* x, int t, const Tw& tw, void* buf, W& w) {
+  typename Tw::Chunk ch[2], chc;
+  tw.issue4(0, ch[0]);  // lands while the first 16-point DFT runs
   if (FLIP) wflip_odd(x, (uint32_t)(t >> 4) << 31);
 #pragma unroll
   for (int m = 1; m < WPTS; ++m) x[m] = cmul(x[m], twist16(m));
@@ -247,12 +261,16 @@ TFB_HD void wfft_forward(cd* x, int t, const Tw& tw, void* buf, W& w) {
 #pragma unroll
   for (int kb = 0; kb < WPTS; kb += 4) {
     cd wk[4];
-    tw.get4(kb, wk);
+    tw.settle4(ch[(kb >> 2) & 1], wk);
+    if (kb + 4 < WPTS)
+      tw.issue4(kb + 4, ch[((kb >> 2) + 1) & 1]);
+    else
+      tw.issue_c(chc);
 #pragma unroll
     for (int j = 0; j < 4; ++j) x[kb + j] = cmul(x[kb + j], wk[j]);
   }
   {
-    const cd c = tw.cc();
+    const cd c = tw.settle_c(chc);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const cd got = w.xchg16(x[8 + j]);
@@ -272,10 +290,13 @@ TFB_HD void wfft_forward(cd* x, int t, const Tw& tw, void* buf, W& w) {
 // FLIP = false: the outputs are left as x[m] (-1)^(m h); the CMux folds the sign into the rounding.
 template <bool FLIP = true, class W, class Tw>
 TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
+  typename Tw::Chunk ch[2], chc;
+  tw.issue_c(chc);
   dft16<-1>(x);
   wexchange<false>(x, t, buf, w);
   {
-    const cd c = tw.cc();
+    const cd c = tw.settle_c(chc);
+    tw.issue4(0, ch[0]);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const cd v = cmulc(x[8 + j], c);
@@ -287,7 +308,8 @@ TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
 #pragma unroll
   for (int kb = 0; kb < WPTS; kb += 4) {
     cd wk[4];
-    tw.get4(kb, wk);
+    tw.settle4(ch[(kb >> 2) & 1], wk);
+    if (kb + 4 < WPTS) tw.issue4(kb + 4, ch[((kb >> 2) + 1) & 1]);
 #pragma unroll
     for (int j = 0; j < 4; ++j) x[kb + j] = cmulc(x[kb + j], wk[j]);
   }
@@ -308,8 +330,8 @@ TFB_HD int wstage_index(int lvl, int q, int c, int t) { return ((lvl * WPTS + q)
 // runs; a Park policy holds them outside the register file between MAC stages (the B200 kernel
 // parks them in tensor memory, which is private per lane and has its own data path), in
 // chunks of PARK_CH values per output polynomial:
-//   load(qb, o0, o1) / store(qb, o0, o1): values qb .. qb+PARK_CH-1 of both polynomials
-//   load_one(c, qb, o): the same of polynomial c only;  flush(): stores are visible to later loads
+//   issue_one(c, qb, chunk) / settle_one(chunk, o): load values qb .. qb+PARK_CH-1 of polynomial c
+//   store(qb, o0, o1): the same values of both polynomials;  flush(): stores are visible to later loads
 //   store_digits / load_digits: the 16 packed level-1 digit words that wait for the second
 //   forward transform of an accumulator polynomial
 #ifndef TFB_PARK_CH
@@ -317,14 +339,15 @@ TFB_HD int wstage_index(int lvl, int q, int c, int t) { return ((lvl * WPTS + q)
 #endif
 constexpr int PARK_CH = TFB_PARK_CH;
 struct RegPark {  // no parking: plain registers (host emulation)
+  typedef MemChunk4 Chunk;
   cd v[2][WPTS];
-  TFB_HD void load_one(int c, int qb, cd* o) const {
+  TFB_HD void issue_one(int c, int qb, Chunk& ch) const {
 #pragma unroll
-    for (int j = 0; j < PARK_CH; ++j) o[j] = v[c][qb + j];
+    for (int j = 0; j < PARK_CH; ++j) ch.v[j] = v[c][qb + j];
   }
-  TFB_HD void load(int qb, cd* o0, cd* o1) const {
-    load_one(0, qb, o0);
-    load_one(1, qb, o1);
+  TFB_HD void settle_one(Chunk& ch, cd* o) const {
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j) o[j] = ch.v[j];
   }
   TFB_HD void store(int qb, const cd* o0, const cd* o1) {
 #pragma unroll
@@ -350,10 +373,23 @@ struct RegPark {  // no parking: plain registers (host emulation)
 template <bool FIRST, class BkSource, class Park>
 TFB_HD void wmac(Park& park, const cd* x, BkSource& bk, const cd* chunk, int t) {
   const cd* key = chunk + t;
+  typename Park::Chunk ch0[2], ch1[2];
+  if (!FIRST) {
+    park.issue_one(0, 0, ch0[0]);
+    park.issue_one(1, 0, ch1[0]);
+  }
 #pragma unroll
   for (int qb = 0; qb < WPTS; qb += PARK_CH) {
     cd o0[PARK_CH], o1[PARK_CH];
-    if (!FIRST) park.load(qb, o0, o1);
+    if (!FIRST) {
+      const int cur = (qb / PARK_CH) & 1;
+      park.settle_one(ch0[cur], o0);
+      park.settle_one(ch1[cur], o1);
+      if (qb + PARK_CH < WPTS) {  // the next chunk travels while this one is multiplied
+        park.issue_one(0, qb + PARK_CH, ch0[cur ^ 1]);
+        park.issue_one(1, qb + PARK_CH, ch1[cur ^ 1]);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < PARK_CH; ++j) {
       const int q = qb + j;
@@ -453,8 +489,13 @@ TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, cons
   TFB_K1D_LOOP
   for (int c = 0; c < 2; ++c) {
     cd x[WPTS];
+    {
+      typename Park::Chunk ch[WPTS / PARK_CH];
 #pragma unroll
-    for (int qb = 0; qb < WPTS; qb += PARK_CH) park.load_one(c, qb, x + qb);
+      for (int qb = 0; qb < WPTS; qb += PARK_CH) park.issue_one(c, qb, ch[qb / PARK_CH]);
+#pragma unroll
+      for (int qb = 0; qb < WPTS; qb += PARK_CH) park.settle_one(ch[qb / PARK_CH], x + qb);
+    }
     wfft_inverse<false>(x, t, tw, buf, w);
     const double sg = (t >> 4) ? -1.0 : 1.0;  // the inverse leaves -x[m] for odd m on the lanes with h = 1
 #pragma unroll
