@@ -408,8 +408,13 @@ constexpr int K1D_HEADER = (int)sizeof(WarpTwiddles) + 4 * 16384 + 128;  // twid
 #endif
 constexpr int WR_SLOTS = TFB_K1D_SLOTS;
 constexpr int WR_CHUNK_BYTES = WCHUNK_CD * (int)sizeof(cd);
-// Non-blocking poll + sleep: a warp that is ahead of the key ring should cost (almost) no issue
-// slots while it waits; the try_wait spin loop executed ~200 instructions per acquire.
+// Waiting for a key chunk: non-blocking mbarrier.test_wait + nanosleep (TFB_K1D_POLL, default), or
+// mbarrier.try_wait with a suspend-time hint.  On real runs a warp waits 2-5 % of the time and polls
+// once or twice per chunk (build with -DTFB_K1D_PROBE to print it); under ncu's instrumentation the
+// loop spins far more, which inflates the instruction counts of a profile.
+#ifndef TFB_K1D_POLL
+#define TFB_K1D_POLL 1  // measured: 68.5 ms (poll) vs 70.8 ms (try_wait) per 14208 gates
+#endif
 __device__ __forceinline__ bool mbar_test_u32(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -424,7 +429,20 @@ __device__ __forceinline__ bool mbar_test_u32(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+#if TFB_K1D_POLL
   while (!mbar_test_u32(bar, parity)) __nanosleep(100);
+#else
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_LOOP:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE;\n"
+      "bra WAIT_LOOP;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar), "r"(parity), "r"(1000000u)  // suspend-time hint: wait in hardware
+      : "memory");
+#endif
 }
 struct WarpRing {
   const cd* bkw;        // full spectral key in global memory
