@@ -1155,13 +1155,14 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
 // Cost model of the four K1 variants (ms per launch on a 148-SM B200 at n = 500, measured with
 // tools/k1_ab.py; only the ratios matter).  Every variant runs in waves of one CTA set per SM:
 //   K1c 1 gate / SM, 1.41 ms per wave        K1a up to 4 gates / SM, 2.49 .. 3.74 ms per wave
-//   K1b 4 gates / SM, 3.35 ms per wave       K1d 12 gates / SM, 9.3 ms per wave
+//   K1b 4 gates / SM, 3.35 ms per wave       K1d 12 gates / SM, 8.6 ms per wave
+constexpr double K1D_WAVE_MS = 8.6;
 static int pick_k1(int64_t k, int sms, double* cost) {
   const double S = (double)sms;
   const double waves_c = ceil(k / S), waves_b = ceil(k / (4 * S)), waves_d = ceil(k / (12 * S));
   const double t[5] = {0.0,
                        k <= S ? 2.49 : (k <= 2 * S ? 2.69 : (k <= 3 * S ? 3.53 : 3.74 * waves_b)),
-                       3.35 * waves_b, 1.41 * waves_c, 9.3 * waves_d};
+                       3.35 * waves_b, 1.41 * waves_c, K1D_WAVE_MS * waves_d};
   int best = 3;
   for (int w = 1; w <= 4; ++w)
     if (t[w] < t[best]) best = w;
@@ -1205,7 +1206,7 @@ static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, int stride, const
   const int w_whole = pick_k1(k, ctx->sm_count, &whole);
   if (body == 0 || rest == 0) return launch_k1_variant(ctx, w_whole, pool, stride, kinds, xr, yr, ext, k, st);
   const int w_tail = pick_k1(rest, ctx->sm_count, &tail);
-  if (9.3 * (double)(body / wave_d) + tail >= whole)
+  if (K1D_WAVE_MS * (double)(body / wave_d) + tail >= whole)
     return launch_k1_variant(ctx, w_whole, pool, stride, kinds, xr, yr, ext, k, st);
   int rc = launch_k1_variant(ctx, 4, pool, stride, kinds, xr, yr, ext, body, st);
   if (rc) return rc;
