@@ -112,6 +112,14 @@ int tfb_debug_key_switch(tfb_ctx *ctx, const uint32_t *ext_dev, void *pool_dev, 
  * un-scaled: double[4][2][512][2] (row, component, frequency, re/im). */
 int tfb_debug_spectral_key(tfb_ctx *ctx, int32_t i, double *out_host);
 
+/* K1 dispatch, host logic only (no GPU needed): which fused-bootstrap variant a launch of k gates
+ * takes on a device with `sms` multiprocessors.  Returns 1 = K1a (one gate per 64-thread CTA),
+ * 2 = K1b (four gates per CTA, TMA key ring), 3 = K1c (one gate over four thread groups: latency),
+ * 4 = K1d (one gate per warp, twelve per CTA: throughput).  When a large launch is split, *body_gates
+ * receives the number of leading gates that run as full K1d waves and the return value is the
+ * variant of the remaining k - *body_gates gates; otherwise *body_gates = 0. */
+int tfb_debug_pick_kernel(int64_t k, int sms, int64_t *body_gates);
+
 /* Number of kernels this context has launched so far (bench `gpu_launches`). */
 int64_t tfb_kernel_launches(const tfb_ctx *ctx);
 

@@ -86,6 +86,7 @@ def lib() -> ctypes.CDLL:
     L.tfb_debug_blind_rotate.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     L.tfb_debug_key_switch.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     L.tfb_debug_spectral_key.argtypes = [_vp, ctypes.c_int32, _vp]
+    L.tfb_debug_pick_kernel.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
     L.tfb_kernel_launches.argtypes = [_vp]
     L.tfb_kernel_launches.restype = ctypes.c_int64
     L.tfb_measure_peaks.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -99,7 +100,7 @@ EXPORTS = (
     "tfb_abi_version", "tfb_last_error", "tfb_ctx_create", "tfb_ctx_destroy", "tfb_load_keys",
     "tfb_gate_launch", "tfb_gate_launch_host", "tfb_rows_negate", "tfb_rows_phase",
     "tfb_debug_blind_rotate", "tfb_debug_key_switch", "tfb_debug_spectral_key",
-    "tfb_kernel_launches", "tfb_measure_peaks",
+    "tfb_debug_pick_kernel", "tfb_kernel_launches", "tfb_measure_peaks",
 )
 
 
@@ -140,6 +141,13 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(self._lib.tfb_kernel_launches(self.handle))
+
+
+def pick_kernel(k: int, sms: int = 148) -> tuple[int, int]:
+    """(variant of the tail or of the whole launch, leading gates that run as full K1d waves)."""
+    body = ctypes.c_int64()
+    which = lib().tfb_debug_pick_kernel(int(k), int(sms), ctypes.byref(body))
+    return int(which), int(body.value)
 
 
 def measure_peaks(device: int = 0) -> dict:

@@ -1196,22 +1196,32 @@ static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, int stri
 // K1 dispatch.  K1c (one gate over four thread groups) wins on latency, K1d (one gate per warp,
 // twelve per SM) on throughput, K1b / K1a in between.  A large launch runs its full K1d waves
 // first and hands the ragged rest to whichever variant finishes it soonest.
+// The split decision of launch_blind_rotate: variant of the tail (or of the whole launch when *body == 0).
+static int plan_k1(int64_t k, int sms, int64_t* body) {
+  const int64_t wave_d = (int64_t)sms * K1D_WARPS;
+  const int64_t full = k / wave_d * wave_d, rest = k - full;
+  double whole = 0, tail = 0;
+  const int w_whole = pick_k1(k, sms, &whole);
+  *body = 0;
+  if (full == 0 || rest == 0) return w_whole;
+  const int w_tail = pick_k1(rest, sms, &tail);
+  if (K1D_WAVE_MS * (double)(full / wave_d) + tail >= whole) return w_whole;
+  *body = full;
+  return w_tail;
+}
+
 static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, int stride, const uint8_t* kinds, const int32_t* xr,
                                const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
   if (ctx->force_kernel)
     return launch_k1_variant(ctx, ctx->force_kernel, pool, stride, kinds, xr, yr, ext, k, st);
-  const int64_t wave_d = (int64_t)ctx->sm_count * K1D_WARPS;
-  const int64_t body = k / wave_d * wave_d, rest = k - body;
-  double whole = 0, tail = 0;
-  const int w_whole = pick_k1(k, ctx->sm_count, &whole);
-  if (body == 0 || rest == 0) return launch_k1_variant(ctx, w_whole, pool, stride, kinds, xr, yr, ext, k, st);
-  const int w_tail = pick_k1(rest, ctx->sm_count, &tail);
-  if (K1D_WAVE_MS * (double)(body / wave_d) + tail >= whole)
-    return launch_k1_variant(ctx, w_whole, pool, stride, kinds, xr, yr, ext, k, st);
-  int rc = launch_k1_variant(ctx, 4, pool, stride, kinds, xr, yr, ext, body, st);
-  if (rc) return rc;
+  int64_t body = 0;
+  const int w_tail = plan_k1(k, ctx->sm_count, &body);
+  if (body) {
+    int rc = launch_k1_variant(ctx, 4, pool, stride, kinds, xr, yr, ext, body, st);
+    if (rc) return rc;
+  }
   return launch_k1_variant(ctx, w_tail, pool, stride, kinds + body, xr + body, yr + body, ext + body * EXT_STRIDE,
-                           rest, st);
+                           k - body, st);
 }
 
 static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, int stride, const int32_t* out_rows,
@@ -1381,6 +1391,14 @@ int tfb_debug_spectral_key(tfb_ctx* ctx, int32_t i, double* out) {
           dst[1] = v.im * HALF_N;
         }
   return TFB_OK;
+}
+
+int tfb_debug_pick_kernel(int64_t k, int sms, int64_t* body_gates) {
+  int64_t body = 0;
+  if (k < 1 || sms < 1) return 0;
+  const int which = plan_k1(k, sms, &body);
+  if (body_gates) *body_gates = body;
+  return which;
 }
 
 int64_t tfb_kernel_launches(const tfb_ctx* ctx) { return ctx ? ctx->launches : 0; }

@@ -23,7 +23,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(library):
     names = declared_symbols()
-    assert len(names) >= 14
+    assert len(names) >= 15
     for name in names:
         assert hasattr(library, name), name
     assert set(names) == set(_cabi.EXPORTS)
@@ -51,6 +51,23 @@ def test_unsupported_parameters_are_rejected_without_a_gpu(library):
     library.tfb_last_error.restype = ctypes.c_char_p
     library.tfb_last_error.argtypes = [ctypes.c_void_p]
     assert b"unsupported" in library.tfb_last_error(None)
+
+
+def test_k1_dispatch_plan(library):
+    """Host-side dispatch of the fused bootstrap (no GPU): latency kernel for narrow launches, the
+    warp-per-gate kernel for wide ones, full K1d waves + a cheaper tail for ragged wide launches."""
+    pick = _cabi.pick_kernel
+    assert pick(1) == (3, 0) and pick(2) == (3, 0) and pick(148) == (3, 0)   # adders / multiplier trees: K1c
+    assert pick(592)[0] == 2 and pick(1184)[0] == 2                           # one / two waves of 4-gate CTAs
+    assert pick(1776) == (4, 0) and pick(3552) == (4, 0)                      # full waves of 12-gate CTAs
+    which, body = pick(1 << 16)                                               # BASELINE configs[1]
+    assert body in (0, 36 * 1776) and (body or which == 4)
+    which, body = pick(2 * 1776 + 300)                                        # ragged: K1d waves, then a short tail
+    assert body == 2 * 1776 and which in (1, 2, 3)
+    for k in (1, 7, 149, 297, 600, 1000, 1777, 5000, 100000):
+        which, body = pick(k)
+        assert which in (1, 2, 3, 4) and 0 <= body < k and body % 1776 == 0
+    assert pick(1776 // 2, sms=74) == (4, 0)                                  # scales with the SM count
 
 
 def test_engine_refuses_to_run_without_cuda(key):
