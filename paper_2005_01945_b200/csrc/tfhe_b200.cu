@@ -8,7 +8,9 @@
 //      K1a k_gate_bootstrap       one gate per 64-thread CTA, key through L1/L2
 //      K1c k_gate_bootstrap_wide  one gate over four thread groups (latency path)
 //   K2 k_key_switch       batched N -> n key switch as an integer rank-8192 update,
-//                         32 ciphertexts x 512 columns per CTA, digits in smem
+//                         32 ciphertexts x 512 columns per CTA, digits in smem (launches < 96 gates)
+//   K2t k_key_switch_mma  the same update as an exact s8 x u8 -> s32 GEMM on the tensor cores
+//                         (tcgen05.mma kind::i8, TMEM accumulator), tfhe_keyswitch_mma.cuh
 //   K3 k_bk_transform     one-time: raw TRGSW rows -> spectral key in K1's register
 //      k_ksk_layout       order; raw key-switching key -> row-padded table
 //   k_rows_negate, k_rows_phase   NOT and batched phase (decryption helper)
@@ -44,6 +46,8 @@ struct tfb_ctx {
   cd* d_bkw = nullptr;         // K1d's staged layout [n][p][lvl][q][c][lane] (cd), prescaled by 1/512
   WarpTwiddles* d_wtw = nullptr;
   int32_t* d_ksk = nullptr;    // [N*t][ROW_STRIDE]
+  uint8_t* d_ksk_mma = nullptr;  // K2t: byte planes as shared-memory images [col tile][K block][32 KB]
+  int force_ks = 0;            // 0 auto, 1 = K2 (IMAD), 2 = K2t (tensor cores)
   Twiddles* d_tw = nullptr;
   uint32_t* d_ext = nullptr;   // scratch [cap][EXT_STRIDE]
   int64_t ext_cap = 0;
@@ -886,6 +890,8 @@ __global__ void k_rows_zero(uint32_t* __restrict__ pool, const int32_t* __restri
   for (int c = threadIdx.x; c <= n; c += blockDim.x) dst[c] = 0u;
 }
 
+#include "tfhe_keyswitch_mma.cuh"
+
 // ------------------------------------------------------------------------------------
 // K3: key setup
 // ------------------------------------------------------------------------------------
@@ -1082,6 +1088,8 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
                              K1B_HEADER + K1B_GROUPS * group_smem(p->n));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gate_bootstrap_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, k1c_smem(p->n));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k2t::k_key_switch_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, k2t::SMEM_BYTES);
   if (e == cudaSuccess) {
     int sms = 0;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1093,6 +1101,7 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
     return TFB_ERR_CUDA;
   }
   if (const char* f = getenv("TFB_FORCE_KERNEL")) ctx->force_kernel = atoi(f);  // A/B switch for profiling
+  if (const char* f = getenv("TFB_FORCE_KS")) ctx->force_ks = atoi(f);
   *out = ctx;
   return TFB_OK;
 }
@@ -1104,6 +1113,7 @@ void tfb_ctx_destroy(tfb_ctx* ctx) {
   cudaFree(ctx->d_bkw);
   cudaFree(ctx->d_wtw);
   cudaFree(ctx->d_ksk);
+  cudaFree(ctx->d_ksk_mma);
   cudaFree(ctx->d_tw);
   cudaFree(ctx->d_ext);
   cudaFree(ctx->d_hx);
@@ -1143,6 +1153,10 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
   k_bk_transform<<<n * BK_ROWS * 2, FFT_THREADS, 0, st>>>(d_bk, ctx->d_bkf, ctx->d_tw);
   k_bk_transform_w<<<n * BK_ROWS * 2, WARP_T, 0, st>>>(d_bk, ctx->d_bkw, ctx->d_wtw);
   k_ksk_layout<<<RING_N * KS_T, 128, 0, st>>>(d_kr, ctx->d_ksk, n);
+  if (!ctx->d_ksk_mma)
+    TFB_CUDA(ctx, cudaMalloc(&ctx->d_ksk_mma, (size_t)k2t::NTILES * k2t::KBLOCKS * k2t::B_BYTES));
+  k2t::k_ksk_mma_layout<<<k2t::NTILES * k2t::KBLOCKS, 256, 0, st>>>(ctx->d_ksk, ctx->d_ksk_mma);
+  ctx->launches += 1;
   ctx->launches += 3;
   TFB_CUDA(ctx, cudaGetLastError());
   TFB_CUDA(ctx, cudaStreamSynchronize(st));
@@ -1226,6 +1240,17 @@ static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, int stride, const
 
 static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, int stride, const int32_t* out_rows,
                              int64_t k, cudaStream_t st) {
+  // K2t (tensor cores) from 96 gates up: 1.6 ms instead of 16.8 ms at 2^16 gates, 0.05 ms for anything up
+  // to ~2000 gates; below, the split IMAD kernel's 0.035 ms is the shorter latency (tools/k2_ab.py)
+  const bool mma = ctx->force_ks ? ctx->force_ks == 2 : k >= 96;
+  if (mma) {
+    const unsigned grid = (unsigned)((k + k2t::M - 1) / k2t::M) * k2t::NTILES;
+    k2t::k_key_switch_mma<<<grid, k2t::THREADS, k2t::SMEM_BYTES, st>>>(ext, ctx->d_ksk_mma, (uint32_t*)pool, out_rows,
+                                                                     stride, ctx->p.n, k);
+    ctx->launches += 1;
+    TFB_CUDA(ctx, cudaGetLastError());
+    return TFB_OK;
+  }
   const unsigned tiles = (unsigned)((k + KS_CT - 1) / KS_CT);
   // small launches: split the 1024 ring coefficients over up to 64 CTAs per tile to fill the chip
   unsigned split = 1;
