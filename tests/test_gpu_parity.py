@@ -141,6 +141,48 @@ def test_every_kernel_variant_is_bit_exact(key, eval_keys, monkeypatch):
         ctx.close()
 
 
+def test_key_switch_on_tensor_cores_is_exact(key, eval_keys, monkeypatch):
+    """K2t (tcgen05.mma kind::i8: digits x byte planes of the key, s32 accumulators in tensor memory)
+    against K2 (IMAD pipe) on arbitrary extracted samples, whole and partial 128-gate tiles, and against
+    the key-switch formula itself: out = (0, b) - sum_r d_r * KSK_r with signed base-4 digits."""
+    import torch
+
+    from paper_2005_01945_b200 import _cabi
+
+    n = key.params.m
+    dev = torch.device("cuda:0")
+    ctxs = {}
+    for mode in ("1", "2"):
+        monkeypatch.setenv("TFB_FORCE_KS", mode)
+        ctxs[mode] = _cabi.Context(0, n, key.params.mu.word, eval_keys.ring)
+        ctxs[mode].call("tfb_load_keys", eval_keys.bk.ctypes.data, eval_keys.ksk.ctypes.data, 0, None)
+    rng = np.random.default_rng(41)
+    ksk = eval_keys.ksk.reshape(-1, n + 1).view(np.uint32)  # [N*t][n+1]
+    for K in (1, 95, 128, 129, 700):
+        ext_h = rng.integers(0, 1 << 32, size=(K, _cabi.EXT_STRIDE), dtype=np.uint32)
+        ext_h[0, :1024] = 0                      # all-zero mask: digits of the rounding bias only
+        ext_h[K - 1, :1024] = 0xFFFFFFFF         # carries through every digit
+        ext = torch.from_numpy(ext_h.view(np.int32)).to(dev)
+        rows = torch.arange(K, dtype=torch.int32, device=dev).flip(0).contiguous()  # scattered output rows
+        outs = {}
+        for mode, ctx in ctxs.items():
+            pool = torch.full((K, _cabi.ROW_STRIDE), 7, dtype=torch.int32, device=dev)
+            ctx.call("tfb_debug_key_switch", ext.data_ptr(), pool.data_ptr(), rows.data_ptr(), K, None)
+            torch.cuda.synchronize()
+            outs[mode] = pool.cpu().numpy().view(np.uint32)
+        assert np.array_equal(outs["1"][:, : n + 1], outs["2"][:, : n + 1]), K
+        for g in (0, K // 2, K - 1):             # the formula, in numpy
+            a = ext_h[g, :1024].astype(np.uint64)
+            bias = (1 << 15) + sum(2 << (32 - 2 * (j + 1)) for j in range(8))
+            ab = (a + bias) % (1 << 32)
+            digits = np.stack([((ab >> (32 - 2 * (j + 1))) & 3).astype(np.int64) - 2 for j in range(8)], axis=1).reshape(-1)
+            want = (-(digits[:, None] * ksk.astype(np.int64)).sum(axis=0)) % (1 << 32)
+            want[n] = (want[n] + int(ext_h[g, 1024])) % (1 << 32)
+            assert np.array_equal(outs["2"][int(rows[g].item()), : n + 1].astype(np.int64), want), (K, g)
+    for ctx in ctxs.values():
+        ctx.close()
+
+
 def test_automatic_dispatch_sizes(gpu, key, eval_keys):
     """Launch sizes on both sides of the K1c / K1a / K1b / K1d dispatch thresholds (2, 4, 12 x SMs)."""
     base = 64
