@@ -557,6 +557,9 @@ struct TmemWPark {
       r[4 * j + 3] = (uint32_t)__double2hiint(o[j].im);
     }
   }
+#ifndef TFB_K1D_ST2
+#define TFB_K1D_ST2 0  // stores only, one double (a natural register pair) per instruction
+#endif
 #ifndef TFB_K1D_ST4
 #define TFB_K1D_ST4 0  // stores only, one complex value per instruction
 #endif
@@ -571,6 +574,11 @@ struct TmemWPark {
                  : "r"(addr)
                  : "memory");
     v = cd{__hiloint2double((int)r1, (int)r0), __hiloint2double((int)r3, (int)r2)};
+  }
+  static __device__ __forceinline__ void st2(uint32_t addr, double v) {  // a register pair is a natural tuple
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr),
+                 "r"((uint32_t)__double2loint(v)), "r"((uint32_t)__double2hiint(v))
+                 : "memory");
   }
   static __device__ __forceinline__ void st4(uint32_t addr, const cd& v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
@@ -628,7 +636,13 @@ struct TmemWPark {
 #endif
   }
   __device__ __forceinline__ void store_one(int c, int qb, const cd* o) const {
-#if TFB_K1D_X4 || TFB_K1D_ST4
+#if TFB_K1D_ST2
+#pragma unroll
+    for (int j = 0; j < PARK_CH; ++j) {
+      st2(taddr + 64 * c + 4 * (qb + j), o[j].re);
+      st2(taddr + 64 * c + 4 * (qb + j) + 2, o[j].im);
+    }
+#elif TFB_K1D_X4 || TFB_K1D_ST4
 #pragma unroll
     for (int j = 0; j < PARK_CH; ++j) st4(taddr + 64 * c + 4 * (qb + j), o[j]);
 #else
