@@ -183,6 +183,31 @@ def test_key_switch_on_tensor_cores_is_exact(key, eval_keys, monkeypatch):
         ctx.close()
 
 
+@pytest.mark.parametrize("n", [7, 511])
+def test_other_lwe_dimensions_through_the_host_path(n, monkeypatch):
+    """The smallest and the largest LWE dimension the library accepts (rows of n + 1 <= 512 words), every
+    K1 / K2 variant and the automatic split dispatch, through tfb_gate_launch_host (packed rows)."""
+    from paper_2005_01945_b200 import LweParams, _cabi, generate_evaluation_keys, keygen
+
+    p = LweParams(m=n)
+    k = keygen(p, seed=3)
+    ek = generate_evaluation_keys(k, seed=3)
+    K = 8
+    xs, ys, kinds, _ = make_inputs(k, K, seed=8, kinds=(np.arange(K) % 8).astype(np.uint8))
+    want = orc.gate_bootstrap_batch(xs, ys, kinds, p.mu.word, ek.bk, ek.ksk, fft=True)
+    for which, ks, count in (("3", "1", 8), ("1", "1", 8), ("2", "2", 200), ("4", "2", 200), ("4", "1", 13), (None, None, 3000)):
+        for name, val in (("TFB_FORCE_KERNEL", which), ("TFB_FORCE_KS", ks)):
+            monkeypatch.setenv(name, val) if val else monkeypatch.delenv(name, raising=False)
+        ctx = _cabi.Context(0, n, p.mu.word, ek.ring)
+        ctx.call("tfb_load_keys", ek.bk.ctypes.data, ek.ksk.ctypes.data, 0, None)
+        idx = np.arange(count) % K
+        xh, yh, kh = (np.ascontiguousarray(a[idx]) for a in (xs, ys, kinds))
+        out = np.zeros((count, n + 1), dtype=np.uint32)
+        ctx.call("tfb_gate_launch_host", xh.ctypes.data, yh.ctypes.data, kh.ctypes.data, out.ctypes.data, count)
+        assert np.array_equal(out, want[idx]), (n, which, ks, count)
+        ctx.close()
+
+
 def test_automatic_dispatch_sizes(gpu, key, eval_keys):
     """Launch sizes on both sides of the K1c / K1a / K1b / K1d dispatch thresholds (2, 4, 12 x SMs)."""
     base = 64
