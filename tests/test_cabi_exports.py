@@ -70,6 +70,30 @@ def test_k1_dispatch_plan(library):
     assert pick(1776 // 2, sms=74) == (4, 0)                                  # scales with the SM count
 
 
+def test_product_path_never_touches_the_oracle():
+    """The oracle is test infrastructure: nothing in the package or in the CUDA sources may import,
+    link or execute anything under oracle/ (only tests/, __graft_entry__.smoke() and the CPU baseline
+    legs of bench.py do)."""
+    import ast
+
+    pkg = os.path.dirname(_cabi.__file__)
+    for name in sorted(os.listdir(pkg)):
+        if not name.endswith(".py"):
+            continue
+        tree = ast.parse(open(os.path.join(pkg, name)).read())
+        for node in ast.walk(tree):
+            mods = []
+            if isinstance(node, ast.Import):
+                mods = [a.name for a in node.names]
+            elif isinstance(node, ast.ImportFrom):
+                mods = [node.module or ""]
+            assert not any(m == "oracle" or m.startswith("oracle.") for m in mods), (name, mods)
+    for name in sorted(os.listdir(_cabi.CSRC)):
+        if name.endswith((".cu", ".cuh")):
+            text = open(os.path.join(_cabi.CSRC, name)).read()
+            assert "oracle/" not in text.replace("the oracle", ""), name  # no include of oracle sources
+
+
 def test_engine_refuses_to_run_without_cuda(key):
     import torch
 
