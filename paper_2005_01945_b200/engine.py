@@ -21,6 +21,7 @@ of the reference (`eval_gate`, `eval_gate_batch`, `eval_compound_batch`,
 from __future__ import annotations
 
 import bisect
+import os
 import enum
 import itertools
 from dataclasses import dataclass, fields, replace
@@ -135,6 +136,8 @@ class RowAllocator:
         self._free_starts: list[int] = []
         self._free_counts: list[int] = []
         self.top = 0  # rows >= top have never been handed out (or were given back)
+        self.hold = False  # while launches are deferred, freed rows wait in quarantine (they may still be read)
+        self._held: list[tuple[int, int]] = []
 
     def alloc(self, count: int) -> RowBlock:
         for i, c in enumerate(self._free_counts):
@@ -150,7 +153,16 @@ class RowAllocator:
         self.top += count
         return RowBlock(self, start, count)
 
+    def end_hold(self) -> None:
+        self.hold = False
+        held, self._held = self._held, []
+        for start, count in held:
+            self._release(start, count)
+
     def _release(self, start: int, count: int) -> None:
+        if self.hold:
+            self._held.append((start, count))
+            return
         starts, counts = self._free_starts, self._free_counts
         i = bisect.bisect_left(starts, start)
         starts.insert(i, start)
@@ -221,6 +233,10 @@ class GateEngine:
         self._bounds = np.zeros(1024, dtype=np.float64)
         self._build_tables()
         self._trivial: dict[int, EncBit] = {}
+        self._deferred: list = []          # launches counted but not yet executed (lazy engines only)
+        self._deferred_gates = 0
+        self._deferred_out = np.zeros(1024, dtype=bool)  # rows some deferred launch will write
+        self.physical_launches = 0         # _evaluate calls (logical launches are stats.batch_launches)
 
     # -- tables ----------------------------------------------------------------------
     def _build_tables(self) -> None:
@@ -401,9 +417,62 @@ class GateEngine:
         self._check_margins(kind_ids, x_rows, y_rows)
         block = self._new_rows(k)
         out_rows = block.rows()
-        self._evaluate(kind_ids, x_rows, y_rows, out_rows)
+        self._submit(kind_ids, x_rows, y_rows, out_rows)
         self._bounds[block.start : block.start + k] = self.fresh_bound
         return out_rows, (block,)
+
+    # -- levelised execution ---------------------------------------------------------------
+    # The reference issues one launch per circuit step (`encirc/scheduler.py:156-171`); its
+    # ripple-carry adder, for instance, is three launches per bit of which the first, (a_i XOR b_i,
+    # a_i AND b_i), does not depend on the carry (`encirc/integers.py:95-113`).  A real bootstrap is
+    # deterministic, so WHEN a launch runs is invisible: a lazy engine counts and checks every launch
+    # at the call (statistics, margins and errors are the reference's) but keeps it in a queue until
+    # a later launch, a NOT, a decryption or a read needs one of its outputs, and then runs the whole
+    # queue -- mutually independent by construction -- as ONE kernel launch.  The adder's dependent
+    # chain shrinks from 3 to 2 kernel launches per bit, the multiplier tree likewise.
+    lazy = False
+    MAX_DEFERRED_GATES = 1 << 20
+    MAX_DEFERRED_LAUNCHES = 256
+
+    def _submit(self, kind_ids, x_rows, y_rows, out_rows) -> None:
+        if not self.lazy:
+            self.physical_launches += 1
+            self._evaluate(kind_ids, x_rows, y_rows, out_rows)
+            return
+        x_rows = np.asarray(x_rows, np.int64)
+        y_rows = np.asarray(y_rows, np.int64)
+        if self._deferred:
+            mask = self._deferred_out
+            top = len(mask)
+            hit = (mask[x_rows[x_rows < top]].any() or mask[y_rows[y_rows < top]].any())
+            if (hit or self._deferred_gates + len(kind_ids) > self.MAX_DEFERRED_GATES
+                    or len(self._deferred) >= self.MAX_DEFERRED_LAUNCHES):
+                self._run_deferred()
+        if len(self._deferred_out) < len(self._bounds):
+            grown = np.zeros(len(self._bounds), dtype=bool)
+            grown[: len(self._deferred_out)] = self._deferred_out
+            self._deferred_out = grown
+        self._alloc.hold = True
+        self._deferred.append((np.array(kind_ids, np.uint8), x_rows.copy(), y_rows.copy(), np.array(out_rows, np.int64)))
+        self._deferred_gates += len(kind_ids)
+        self._deferred_out[out_rows] = True
+
+    def _run_deferred(self) -> None:
+        """Execute every queued launch as one.  Called before anything reads or rewrites rows."""
+        if not self._deferred:
+            return
+        queue, self._deferred, self._deferred_gates = self._deferred, [], 0
+        for _, _, _, out in queue:
+            self._deferred_out[out] = False
+        if len(queue) == 1:
+            kinds, xs, ys, outs = queue[0]
+        else:
+            kinds, xs, ys, outs = (np.concatenate([q[j] for q in queue]) for j in range(4))
+        self.physical_launches += 1
+        try:
+            self._evaluate(kinds, xs, ys, outs)
+        finally:
+            self._alloc.end_hold()
 
     def bootstrap(self, bit: EncBit) -> EncBit:
         """Standalone refresh; precondition noise_bound < mu, one launch."""
@@ -549,6 +618,7 @@ class B200Engine(GateEngine):
 
     name = "b200-tfhe"
     _ENC_STREAM = 0
+    lazy = os.environ.get("TFB_EAGER", "0") in ("", "0")  # TFB_EAGER=1: one kernel launch per logical launch
 
     def __init__(self, key: SecretKey, seed: int = 0, pool: WorkerPool | None = None, *,
                  device: int | None = None, ring=None, eval_keys=None, initial_rows: int = 4096):
@@ -592,6 +662,9 @@ class B200Engine(GateEngine):
         self._pool_t = grown
 
     def _flush(self) -> None:
+        """Bring device storage up to date: queued launches first (their inputs' uploads happen inside),
+        then host words waiting for upload."""
+        self._run_deferred()
         if not self._pending:
             return
         torch, n1 = self._torch, self.params.m + 1
@@ -614,7 +687,7 @@ class B200Engine(GateEngine):
                            base + 2 * step, k, self._stream())
 
     def _refresh(self, in_rows, out_rows) -> None:
-        self._evaluate(np.full(len(in_rows), IDENTITY_KIND_ID, np.uint8), in_rows, in_rows, out_rows)
+        self._submit(np.full(len(in_rows), IDENTITY_KIND_ID, np.uint8), in_rows, in_rows, out_rows)
 
     def _negate_rows(self, rows):
         self._flush()
@@ -701,4 +774,5 @@ class B200Engine(GateEngine):
         return self._ctx.kernel_launches
 
     def synchronize(self) -> None:
+        self._flush()
         self._torch.cuda.synchronize(self.device)

@@ -13,9 +13,10 @@ from paper_2005_01945_b200.torus import LweSample, gaussian_noise_words, uniform
 class HostOracleEngine(GateEngine):
     name = "host-oracle-tfhe"
 
-    def __init__(self, key, seed=0, pool=None):
+    def __init__(self, key, seed=0, pool=None, lazy=False):
         self._words = np.zeros((1024, key.params.m + 1), dtype=np.uint32)
         super().__init__(key.params, pool)
+        self.lazy = bool(lazy)  # levelised execution (GateEngine._submit), as B200Engine runs by default
         self.key, self.seed = key, int(seed)
         self._enc_rng = np.random.default_rng((self.seed, 0))
         self.eval_keys = generate_evaluation_keys(key, self.seed)
@@ -32,9 +33,10 @@ class HostOracleEngine(GateEngine):
             self.eval_keys.bk, self.eval_keys.ksk, fft=True)
 
     def _refresh(self, in_rows, out_rows):
-        self._evaluate(np.full(len(in_rows), IDENTITY_KIND_ID, np.uint8), in_rows, in_rows, out_rows)
+        self._submit(np.full(len(in_rows), IDENTITY_KIND_ID, np.uint8), in_rows, in_rows, out_rows)
 
     def _negate_rows(self, rows):
+        self._run_deferred()
         block = self._new_rows(len(rows))
         out = block.rows()
         self._words[out] = (0 - self._words[rows]).astype(np.uint32)
@@ -58,6 +60,7 @@ class HostOracleEngine(GateEngine):
         return out, (block,)
 
     def decrypt_rows(self, rows):
+        self._run_deferred()
         rows = np.asarray(rows, np.int64)
         self._check_decryptable(rows)
         w = self._words[rows]
@@ -65,6 +68,7 @@ class HostOracleEngine(GateEngine):
         return ((ph > 0) & (ph < np.uint32(self.params.half_word))).astype(np.int64)
 
     def read_rows(self, rows):
+        self._run_deferred()
         return self._words[np.asarray(rows, np.int64)].copy()
 
     def write_rows(self, words, bounds):
@@ -80,5 +84,6 @@ class HostOracleEngine(GateEngine):
         return int(rows[0]), owners
 
     def _row_sample(self, row):
+        self._run_deferred()
         w = self._words[row]
         return LweSample(w[:-1].copy(), int(w[-1]), float(self._bounds[row]), self.params.w)

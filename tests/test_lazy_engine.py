@@ -1,0 +1,93 @@
+"""Levelised (deferred) launch execution of GateEngine: a lazy engine counts and checks every launch at
+the call, runs queued launches as one kernel launch when a result is needed, and must be
+indistinguishable from the eager engine in results, ciphertext words, statistics and errors.
+Exercised on CPU with the host oracle engine (real bootstraps by the C oracle, small LWE dimension)."""
+import gc
+
+import numpy as np
+import pytest
+
+from paper_2005_01945_b200 import (
+    BootstrapMarginError, GateKind, LweParams, PoolConfig, WorkerPool, add_bitwise, decrypt_int, decrypt_vector,
+    encrypt_int, encrypt_vector, keygen, mul_naive, vec_add,
+)
+from tests.host_engine import HostOracleEngine
+
+
+@pytest.fixture(scope="module")
+def small_key():
+    return keygen(LweParams(m=20), seed=5)
+
+
+def engines(key):
+    pool = lambda: WorkerPool(PoolConfig(workers=1, max_batch=1 << 16))
+    eager = HostOracleEngine(key, seed=3, pool=pool(), lazy=False)
+    lazy = HostOracleEngine(key, seed=3, pool=pool(), lazy=True)
+    lazy.eval_keys = eager.eval_keys
+    return eager, lazy
+
+
+def test_lazy_engine_is_indistinguishable_and_launches_less(small_key):
+    eager, lazy = engines(small_key)
+    outs = {}
+    for eng in (eager, lazy):
+        x, y = encrypt_int(eng, 0xB7, 8), encrypt_int(eng, 0x5D, 8)
+        eng.reset_stats()
+        eng.physical_launches = 0
+        s = add_bitwise(x, y)
+        p = mul_naive(encrypt_int(eng, 11, 4), encrypt_int(eng, 13, 4))
+        v = vec_add(encrypt_vector(eng, [3, 200, 77], 8), encrypt_vector(eng, [250, 100, 9], 8))
+        rec = eng.stats.as_record()
+        words = eng.read_rows([b.row for b in s.bits] + [b.row for b in p.bits])
+        outs[eng.lazy] = (decrypt_int(eng, s), decrypt_int(eng, p), decrypt_vector(eng, v), rec, words,
+                          eng.physical_launches)
+    e, l = outs[False], outs[True]
+    assert e[0] == l[0] == (0xB7 + 0x5D) % 256 and e[1] == l[1] == 143 and e[2] == l[2] == [253, 44, 86]
+    assert e[3] == l[3]                       # the reference's counters do not see the deferral
+    assert np.array_equal(e[4], l[4])         # nor do the ciphertexts: a bootstrap draws no randomness
+    assert e[5] == e[3]["batch_launches"]     # eager: one kernel launch per logical launch
+    assert l[5] < 0.75 * e[5]                 # lazy: the carry-independent launches ride along
+
+
+def test_adder_chain_is_two_kernel_launches_per_bit(small_key):
+    _, lazy = engines(small_key)
+    n = 6
+    x, y = encrypt_int(lazy, 41, n), encrypt_int(lazy, 22, n)
+    lazy.reset_stats()
+    lazy.physical_launches = 0
+    s = add_bitwise(x, y)
+    assert lazy.stats.batch_launches == 3 * n
+    assert decrypt_int(lazy, s) == 63
+    assert lazy.physical_launches == 2 * n + 1
+
+
+def test_rows_freed_while_a_launch_is_queued_are_not_recycled(small_key):
+    _, lazy = engines(small_key)
+    # inputs die right after the call, while the launch is still queued ...
+    out = lazy.eval_gate(GateKind.AND, lazy.encrypt(1), lazy.encrypt(1))
+    gc.collect()
+    assert lazy._deferred and lazy._alloc.hold
+    # ... and fresh allocations must not land on their rows before the launch has run
+    fresh = [lazy.encrypt(0) for _ in range(8)]
+    assert lazy.decrypt(out) == 1 and not lazy._deferred and not lazy._alloc.hold
+    assert [lazy.decrypt(b) for b in fresh] == [0] * 8
+    # a queued launch whose result is dropped still runs (or not) without disturbing later ones
+    lazy.eval_gate(GateKind.XOR, lazy.encrypt(1), lazy.encrypt(0))
+    gc.collect()
+    keep = lazy.eval_gate(GateKind.OR, lazy.encrypt(0), lazy.encrypt(1))
+    assert lazy.decrypt(keep) == 1
+
+
+def test_not_bootstrap_and_margin_errors_with_queued_launches(small_key):
+    eager, lazy = engines(small_key)
+    for eng in (eager, lazy):
+        a, b = eng.encrypt(1), eng.encrypt(0)
+        g = eng.eval_gate(GateKind.NAND, a, b)            # queued on the lazy engine
+        assert eng.decrypt(eng.eval_not(g)) == 0           # NOT reads the row: the queue runs first
+        r = eng.bootstrap(eng.eval_gate(GateKind.OR, a, b))
+        assert eng.decrypt(r) == 1 and r.noise_bound == eng.fresh_bound
+        noisy = eng.eval_gate(GateKind.AND, a, a)
+        eng._bounds[noisy.row] = 0.2                       # over-noised by hand, as the reference's tests do
+        with pytest.raises(BootstrapMarginError):          # raised at the call, not when the queue runs
+            eng.eval_gate(GateKind.AND, noisy, a)
+        assert eng.decrypt(eng.eval_gate(GateKind.XOR, a, b)) == 1

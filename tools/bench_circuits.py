@@ -30,7 +30,8 @@ ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "circuits.json
 args = ap.parse_args()
 
 key = keygen(LweParams(), seed=2024)
-eng = B200Engine(key, seed=42, pool=WorkerPool(PoolConfig(workers=1, max_batch=1 << 23)))
+eng = B200Engine(key, seed=42, pool=WorkerPool(PoolConfig(workers=1, max_batch=1 << 23)),
+                 initial_rows=1 << 18)  # 512 MB of rows up front: pool growth (a cudaMalloc) stays out of the timed regions
 rng = np.random.default_rng((42, 2))
 rows = []
 
