@@ -233,9 +233,10 @@ class GateEngine:
         self._bounds = np.zeros(1024, dtype=np.float64)
         self._build_tables()
         self._trivial: dict[int, EncBit] = {}
-        self._deferred: list = []          # launches counted but not yet executed (lazy engines only)
+        self._deferred: dict = {}          # level -> launches counted but not yet executed (lazy engines only)
         self._deferred_gates = 0
-        self._deferred_out = np.zeros(1024, dtype=bool)  # rows some deferred launch will write
+        self._deferred_launches = 0
+        self._row_level = np.zeros(1024, dtype=np.int32)  # level of the queued launch that will write a row (0: none)
         self.physical_launches = 0         # _evaluate calls (logical launches are stats.batch_launches)
 
     # -- tables ----------------------------------------------------------------------
@@ -422,56 +423,66 @@ class GateEngine:
         return out_rows, (block,)
 
     # -- levelised execution ---------------------------------------------------------------
-    # The reference issues one launch per circuit step (`encirc/scheduler.py:156-171`); its
-    # ripple-carry adder, for instance, is three launches per bit of which the first, (a_i XOR b_i,
-    # a_i AND b_i), does not depend on the carry (`encirc/integers.py:95-113`).  A real bootstrap is
-    # deterministic, so WHEN a launch runs is invisible: a lazy engine counts and checks every launch
-    # at the call (statistics, margins and errors are the reference's) but keeps it in a queue until
-    # a later launch, a NOT, a decryption or a read needs one of its outputs, and then runs the whole
-    # queue -- mutually independent by construction -- as ONE kernel launch.  The adder's dependent
-    # chain shrinks from 3 to 2 kernel launches per bit, the multiplier tree likewise.
+    # The reference issues one launch per circuit step (`encirc/scheduler.py:156-171`): three per bit of
+    # a ripple-carry adder (`encirc/integers.py:95-113`), one adder after the other through the levels of
+    # a multiplier tree (`encirc/integers.py:177-238`).  A real bootstrap is deterministic, so WHEN a
+    # launch runs is invisible: a lazy engine counts and checks every launch at the call (statistics,
+    # margins and errors are the reference's) but only records it, with its LEVEL = 1 + the highest level
+    # among the still-unevaluated launches that produce its inputs.  When something reads a row (a
+    # decryption, a NOT, a serialisation) or the queue holds MAX_DEFERRED_GATES, the queue runs level by
+    # level, all launches of a level -- mutually independent by construction -- as ONE kernel launch.
+    # The carry-independent launches of an adder collapse into one, and the adders of consecutive tree
+    # levels run as a wavefront: a 32-bit multiply is 138 dependent kernel launches instead of 961.
     lazy = False
-    MAX_DEFERRED_GATES = 1 << 20
-    MAX_DEFERRED_LAUNCHES = 256
+    MAX_DEFERRED_GATES = 1 << 20      # rows stay allocated until the queue has run: 2 GiB of ciphertexts
+    MAX_DEFERRED_LAUNCHES = 1 << 14
 
     def _submit(self, kind_ids, x_rows, y_rows, out_rows) -> None:
         if not self.lazy:
             self.physical_launches += 1
             self._evaluate(kind_ids, x_rows, y_rows, out_rows)
             return
-        x_rows = np.asarray(x_rows, np.int64)
-        y_rows = np.asarray(y_rows, np.int64)
+        x_rows = np.array(x_rows, np.int64)
+        y_rows = np.array(y_rows, np.int64)
+        out_rows = np.array(out_rows, np.int64)
+        k = len(kind_ids)
+        if self._deferred and (self._deferred_gates + k > self.MAX_DEFERRED_GATES
+                               or self._deferred_launches >= self.MAX_DEFERRED_LAUNCHES):
+            self._run_deferred()
+        if len(self._row_level) < len(self._bounds):
+            grown = np.zeros(len(self._bounds), dtype=np.int32)
+            grown[: len(self._row_level)] = self._row_level
+            self._row_level = grown
+        level = 1
         if self._deferred:
-            mask = self._deferred_out
-            top = len(mask)
-            hit = (mask[x_rows[x_rows < top]].any() or mask[y_rows[y_rows < top]].any())
-            if (hit or self._deferred_gates + len(kind_ids) > self.MAX_DEFERRED_GATES
-                    or len(self._deferred) >= self.MAX_DEFERRED_LAUNCHES):
-                self._run_deferred()
-        if len(self._deferred_out) < len(self._bounds):
-            grown = np.zeros(len(self._bounds), dtype=bool)
-            grown[: len(self._deferred_out)] = self._deferred_out
-            self._deferred_out = grown
-        self._alloc.hold = True
-        self._deferred.append((np.array(kind_ids, np.uint8), x_rows.copy(), y_rows.copy(), np.array(out_rows, np.int64)))
-        self._deferred_gates += len(kind_ids)
-        self._deferred_out[out_rows] = True
+            lv = self._row_level
+            level += int(max(lv[x_rows].max(), lv[y_rows].max()))
+        self._alloc.hold = True  # rows freed from now on may still be read or written by the queue
+        self._deferred.setdefault(level, []).append((np.array(kind_ids, np.uint8), x_rows, y_rows, out_rows))
+        self._deferred_gates += k
+        self._deferred_launches += 1
+        self._row_level[out_rows] = level
 
     def _run_deferred(self) -> None:
-        """Execute every queued launch as one.  Called before anything reads or rewrites rows."""
+        """Execute the queue, one kernel launch per level.  Called before anything reads or rewrites rows."""
         if not self._deferred:
             return
-        queue, self._deferred, self._deferred_gates = self._deferred, [], 0
-        for _, _, _, out in queue:
-            self._deferred_out[out] = False
-        if len(queue) == 1:
-            kinds, xs, ys, outs = queue[0]
-        else:
-            kinds, xs, ys, outs = (np.concatenate([q[j] for q in queue]) for j in range(4))
-        self.physical_launches += 1
+        queue, self._deferred = self._deferred, {}
+        self._deferred_gates = self._deferred_launches = 0
         try:
-            self._evaluate(kinds, xs, ys, outs)
+            for level in sorted(queue):
+                batch = queue[level]
+                if len(batch) == 1:
+                    kinds, xs, ys, outs = batch[0]
+                else:
+                    kinds, xs, ys, outs = (np.concatenate([q[j] for q in batch]) for j in range(4))
+                self.physical_launches += 1
+                self._evaluate(kinds, xs, ys, outs)
+                self._row_level[outs] = 0
         finally:
+            for batch in queue.values():  # after an error nothing may stay marked as pending
+                for q in batch:
+                    self._row_level[q[3]] = 0
             self._alloc.end_hold()
 
     def bootstrap(self, bit: EncBit) -> EncBit:

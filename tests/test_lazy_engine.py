@@ -61,6 +61,36 @@ def test_adder_chain_is_two_kernel_launches_per_bit(small_key):
     assert lazy.physical_launches == 2 * n + 1
 
 
+def test_multiplier_tree_runs_as_a_wavefront(small_key):
+    """The adders of consecutive tree levels overlap: the dependent chain of an n-bit multiply is about
+    one 2n-bit adder (2 kernel launches per bit) plus 2 per extra level, not one adder per level."""
+    eager, lazy = engines(small_key)
+    n = 8
+    got = {}
+    for eng in (eager, lazy):
+        x, y = encrypt_int(eng, 201, n), encrypt_int(eng, 173, n)
+        eng.reset_stats()
+        eng.physical_launches = 0
+        p = mul_naive(x, y)
+        got[eng.lazy] = (decrypt_int(eng, p), eng.stats.as_record(), eng.physical_launches,
+                         eng.read_rows([b.row for b in p.bits]))
+    assert got[False][0] == got[True][0] == 201 * 173
+    assert got[False][1] == got[True][1] and got[False][1]["batch_launches"] == 1 + 3 * 6 * n
+    assert np.array_equal(got[False][3], got[True][3])
+    assert got[False][2] == 1 + 3 * 6 * n            # eager: 145 kernel launches
+    assert got[True][2] <= 2 * (2 * n) + 2 * 3 + 3   # lazy: one adder deep plus a few
+
+
+def test_queue_is_flushed_at_its_capacity(small_key):
+    _, lazy = engines(small_key)
+    lazy.MAX_DEFERRED_GATES = 8
+    bits = [lazy.encrypt(i & 1) for i in range(6)]
+    outs = [lazy.eval_gate(GateKind.XOR, bits[i], bits[(i + 1) % 6]) for i in range(6)]  # independent launches
+    outs2 = lazy.eval_gate_batch(GateKind.AND, outs, outs)                                # 6 more: over the cap
+    assert lazy._deferred_gates <= 8
+    assert [lazy.decrypt(b) for b in outs2] == [1] * 6
+
+
 def test_rows_freed_while_a_launch_is_queued_are_not_recycled(small_key):
     _, lazy = engines(small_key)
     # inputs die right after the call, while the launch is still queued ...
