@@ -632,7 +632,7 @@ class B200Engine(GateEngine):
     lazy = os.environ.get("TFB_EAGER", "0") in ("", "0")  # TFB_EAGER=1: one kernel launch per logical launch
 
     def __init__(self, key: SecretKey, seed: int = 0, pool: WorkerPool | None = None, *,
-                 device: int | None = None, ring=None, eval_keys=None, initial_rows: int = 4096):
+                 device: int | None = None, ring=None, eval_keys=None, initial_rows: int = 1 << 16):
         import torch  # device memory + streams only
 
         from . import _cabi
