@@ -265,6 +265,7 @@ class GateEngine:
         self._absx = np.abs(coeffs[:, 0]).astype(np.float64)
         self._absy = np.abs(coeffs[:, 1]).astype(np.float64)
         self._margins = np.array(margins)
+        self._safe_bound = float(np.min(self._margins / (self._absx + self._absy)))
         self._truth = np.array([_GATES[k][0] for k in TWO_INPUT_KINDS], dtype=np.uint8)
 
     def gate_margin(self, kind: GateKind) -> float:
@@ -296,7 +297,11 @@ class GateEngine:
         st.largest_batch = max(st.largest_batch, k)
 
     def _check_margins(self, kind_ids: np.ndarray, x_rows: np.ndarray, y_rows: np.ndarray) -> None:
-        load = self._absx[kind_ids] * self._bounds[x_rows] + self._absy[kind_ids] * self._bounds[y_rows]
+        bx, by = self._bounds[x_rows], self._bounds[y_rows]
+        # every kind passes when both bounds are below margin / (|cx| + |cy|): the common case, two reductions
+        if max(bx.max(), by.max()) < self._safe_bound:
+            return
+        load = self._absx[kind_ids] * bx + self._absy[kind_ids] * by
         room = self._margins[kind_ids]
         if np.any(load >= room):
             j = int(np.argmax(load - room))
