@@ -44,8 +44,9 @@ class tfb_params(ctypes.Structure):
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
     """Compile csrc/tfhe_b200.cu for sm_100a into csrc/libtfhe_b200.so."""
-    srcs = [os.path.join(CSRC, f) for f in ("tfhe_b200.cu", "tfhe_device.cuh")]
-    srcs.append(os.path.join(INCLUDE, "tfhe_b200.h"))
+    # every source the translation unit can include: all of csrc/ plus the public headers
+    srcs = [os.path.join(d, f) for d in (CSRC, INCLUDE) for f in sorted(os.listdir(d))
+            if f.endswith((".cu", ".cuh", ".h"))]
     fresh = os.path.exists(LIB_PATH) and all(os.path.getmtime(LIB_PATH) >= os.path.getmtime(s) for s in srcs)
     if fresh and not force:
         return LIB_PATH

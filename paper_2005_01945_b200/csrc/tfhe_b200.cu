@@ -75,6 +75,26 @@ static thread_local std::string g_create_err;
     }                                                                                  \
   } while (0)
 
+// Every entry point runs on the context's device and leaves the caller's current device as it
+// found it (a process may drive several engines / GPUs).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err;
+  explicit DeviceGuard(int device) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != device)
+      err = cudaSetDevice(device);
+    else
+      prev = -1;  // nothing to restore
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+#define TFB_ENTER(ctx)                     \
+  DeviceGuard guard_((ctx)->device);       \
+  TFB_CUDA(ctx, guard_.err)
+
 struct BlockSync {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
@@ -222,55 +242,6 @@ constexpr int K1B_SLOTS = TFB_K1B_SLOTS;
 // dynamic smem: twiddles | ring[K1B_SLOTS][STAGE_CD] | mbarriers (64 B) | groups
 constexpr int K1B_HEADER = (int)sizeof(Twiddles) + K1B_SLOTS * STAGE_BYTES + 64;
 
-// ---- tensor-memory parking of the CMux accumulators ------------------------------------
-// TMEM (256 KB per SM) is reachable only through tcgen05.ld/st; with the 32x32b shape thread
-// i of a warp owns lane 32*(warp%4)+i and any columns, i.e. it is private per-thread storage
-// the size of the register file.  Between the two halves of a CMux the 16 complex
-// accumulators of a thread (64 words) are parked there, which removes them from the
-// register budget of the second paired transform.
-#ifndef TFB_K1B_TMEM
-#define TFB_K1B_TMEM 0  // measured: 6 groups x 168 regs with parked accumulators = 4 groups x 255 regs without (93.9 vs 93.6 ms per 16 Ki gates)
-#endif
-struct TmemPark {
-  static constexpr bool parks = true;
-  uint32_t taddr;  // (lane << 16) | first column of this warp's 64-column slice
-  __device__ __forceinline__ void store(const cd* o0, const cd* o1) {
-    uint32_t r[64];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      r[8 * k + 0] = (uint32_t)__double2loint(o0[k].re);
-      r[8 * k + 1] = (uint32_t)__double2hiint(o0[k].re);
-      r[8 * k + 2] = (uint32_t)__double2loint(o0[k].im);
-      r[8 * k + 3] = (uint32_t)__double2hiint(o0[k].im);
-      r[8 * k + 4] = (uint32_t)__double2loint(o1[k].re);
-      r[8 * k + 5] = (uint32_t)__double2hiint(o1[k].re);
-      r[8 * k + 6] = (uint32_t)__double2loint(o1[k].im);
-      r[8 * k + 7] = (uint32_t)__double2hiint(o1[k].im);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)  // four 16-column stores
-      asm volatile(
-          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-          "%14, %15, %16};" ::"r"(taddr + 16 * q),
-          "r"(r[16 * q + 0]), "r"(r[16 * q + 1]), "r"(r[16 * q + 2]), "r"(r[16 * q + 3]), "r"(r[16 * q + 4]),
-          "r"(r[16 * q + 5]), "r"(r[16 * q + 6]), "r"(r[16 * q + 7]), "r"(r[16 * q + 8]), "r"(r[16 * q + 9]),
-          "r"(r[16 * q + 10]), "r"(r[16 * q + 11]), "r"(r[16 * q + 12]), "r"(r[16 * q + 13]), "r"(r[16 * q + 14]),
-          "r"(r[16 * q + 15])
-          : "memory");
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  }
-  __device__ __forceinline__ void load(int k2, cd& o0, cd& o1) {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr + 8 * k2)
-                 : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    o0 = cd{__hiloint2double((int)r[1], (int)r[0]), __hiloint2double((int)r[3], (int)r[2])};
-    o1 = cd{__hiloint2double((int)r[5], (int)r[4]), __hiloint2double((int)r[7], (int)r[6])};
-  }
-};
-
 struct RingBk {
   const cd* bkf;       // full spectral key in global memory
   cd* ring;            // K1B_SLOTS stages in shared memory
@@ -355,30 +326,8 @@ __global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
   const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
   uint32_t* dst = want < k ? ext + g * EXT_STRIDE : reinterpret_cast<uint32_t*>(s0);  // scratch sink
   GroupSync sync{grp + 1};
-#if TFB_K1B_TMEM
-  // 64 columns per warp; warps w, w+4, w+8, ... share a lane quarter and take consecutive slices
-  constexpr uint32_t kTmemCols = (K1B_THREADS / 128) * 64 <= 64 ? 64 : ((K1B_THREADS / 128) * 64 <= 128 ? 128 : 256);
-  __shared__ uint32_t tmem_base;
-  const uint32_t warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "n"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  TmemPark park{tmem_base + (((warp & 3u) * 32u) << 16) + (warp >> 2) * 64u};
-  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, dst, t, sync, park);
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols) : "memory");
-#else
   NoPark park;
   gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, dst, t, sync, park);
-#endif
 }
 
 // ------------------------------------------------------------------------------------
@@ -484,9 +433,17 @@ struct WarpRing {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
       const int sl = slot(chunk);
-      if (atomicAdd(&released[sl], 1u) == (uint32_t)(K1D_WARPS - 1)) {  // last one out refills the slot
+      // acq_rel: the counter chains every warp's (generic-proxy) reads of the slot before the last
+      // arriver, whose proxy fence then orders them before the async-proxy refill (PTX memory model:
+      // a write-after-read across proxies needs both)
+      uint32_t before;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(before)
+                   : "r"(smem_u32(&released[sl]))
+                   : "memory");
+      if (before == (uint32_t)(K1D_WARPS - 1)) {  // last one out refills the slot
         released[sl] = 0;
-        __threadfence_block();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (chunk + WR_SLOTS < n_chunks) issue(chunk + WR_SLOTS);
       }
     }
@@ -557,95 +514,7 @@ struct TmemWPark {
       r[4 * j + 3] = (uint32_t)__double2hiint(o[j].im);
     }
   }
-#ifndef TFB_K1D_ST2
-#define TFB_K1D_ST2 0  // stores only, one double (a natural register pair) per instruction
-#endif
-#ifndef TFB_K1D_ST4
-#define TFB_K1D_ST4 0  // stores only, one complex value per instruction
-#endif
-#ifndef TFB_K1D_X4
-#define TFB_K1D_X4 0  // 1: move accumulators one complex value (4 columns) per instruction (a 4-register tuple is
-                      // a natural aligned quad; 16-register tuples cost a MOV per word) -- measured slower: 83.8 vs 73.2 ms
-#endif
-  static __device__ __forceinline__ void ld4(uint32_t addr, cd& v) {
-    uint32_t r0, r1, r2, r3;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr)
-                 : "memory");
-    v = cd{__hiloint2double((int)r1, (int)r0), __hiloint2double((int)r3, (int)r2)};
-  }
-  static __device__ __forceinline__ void st2(uint32_t addr, double v) {  // a register pair is a natural tuple
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr),
-                 "r"((uint32_t)__double2loint(v)), "r"((uint32_t)__double2hiint(v))
-                 : "memory");
-  }
-  static __device__ __forceinline__ void st4(uint32_t addr, const cd& v) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
-                 "r"((uint32_t)__double2loint(v.re)), "r"((uint32_t)__double2hiint(v.re)),
-                 "r"((uint32_t)__double2loint(v.im)), "r"((uint32_t)__double2hiint(v.im))
-                 : "memory");
-  }
-  // the wait makes the loaded registers valid; tying them to it keeps their uses behind it
-  static __device__ __forceinline__ void wait_ld4(cd* o) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+d"(o[0].re), "+d"(o[0].im), "+d"(o[1].re), "+d"(o[1].im), "+d"(o[2].re), "+d"(o[2].im),
-                   "+d"(o[3].re), "+d"(o[3].im)::"memory");
-  }
-  __device__ __forceinline__ void load_one(int c, int qb, cd* o) const {
-#if TFB_K1D_X4
-#pragma unroll
-    for (int j = 0; j < PARK_CH; ++j) ld4(taddr + 64 * c + 4 * (qb + j), o[j]);
-    wait_ld4(o);
-#else
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%16];\n\ttcgen05.wait::ld.sync.aligned;"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr + 64 * c + 4 * qb)
-        : "memory");
-    unpack(r, o);
-#endif
-  }
-  __device__ __forceinline__ void load(int qb, cd* o0, cd* o1) const {
-#if TFB_K1D_X4
-#pragma unroll
-    for (int j = 0; j < PARK_CH; ++j) {
-      ld4(taddr + 4 * (qb + j), o0[j]);
-      ld4(taddr + 64 + 4 * (qb + j), o1[j]);
-    }
-    wait_ld4(o0);
-    wait_ld4(o1);
-#else
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%32];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
-        "%30, %31}, [%33];\n\ttcgen05.wait::ld.sync.aligned;"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr + 4 * qb), "r"(taddr + 64 + 4 * qb)
-        : "memory");
-    unpack(r, o0);
-    unpack(r + 16, o1);
-#endif
-  }
   __device__ __forceinline__ void store_one(int c, int qb, const cd* o) const {
-#if TFB_K1D_ST2
-#pragma unroll
-    for (int j = 0; j < PARK_CH; ++j) {
-      st2(taddr + 64 * c + 4 * (qb + j), o[j].re);
-      st2(taddr + 64 * c + 4 * (qb + j) + 2, o[j].im);
-    }
-#elif TFB_K1D_X4 || TFB_K1D_ST4
-#pragma unroll
-    for (int j = 0; j < PARK_CH; ++j) st4(taddr + 64 * c + 4 * (qb + j), o[j]);
-#else
     uint32_t r[16];
     pack(o, r);
     asm volatile(
@@ -654,7 +523,6 @@ struct TmemWPark {
         "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
         "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
-#endif
   }
   __device__ __forceinline__ void store(int qb, const cd* o0, const cd* o1) const {
     store_one(0, qb, o0);
@@ -703,25 +571,6 @@ struct TmemTw {
   __device__ __forceinline__ cd settle_c(Chunk& ch) const {
     asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(ch.r[0]), "+r"(ch.r[1]), "+r"(ch.r[2]), "+r"(ch.r[3])::"memory");
     return cd{__hiloint2double((int)ch.r[1], (int)ch.r[0]), __hiloint2double((int)ch.r[3], (int)ch.r[2])};
-  }
-  __device__ __forceinline__ void get4(int kb, cd* w) const {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%16];\n\ttcgen05.wait::ld.sync.aligned;"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr + 4 * kb)
-        : "memory");
-    TmemWPark::unpack(r, w);
-  }
-  __device__ __forceinline__ cd cc() const {
-    uint32_t r[4];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n\ttcgen05.wait::ld.sync.aligned;"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(taddr + 64)
-                 : "memory");
-    return cd{__hiloint2double((int)r[1], (int)r[0]), __hiloint2double((int)r[3], (int)r[2])};
   }
   // one warp per lane quarter writes the table
   __device__ __forceinline__ void fill(const LaneTwiddles& lt) const {
@@ -1072,7 +921,8 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
     g_create_err = "unsupported parameter set (compiled: N=1024 l=2 Bgbit=10 t=8 basebit=2, n<=511)";
     return TFB_ERR_INVALID;
   }
-  cudaError_t e = cudaSetDevice(device);
+  DeviceGuard guard(device);
+  cudaError_t e = guard.err;
   if (e != cudaSuccess) {
     g_create_err = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
     return TFB_ERR_CUDA;
@@ -1122,7 +972,7 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
 
 void tfb_ctx_destroy(tfb_ctx* ctx) {
   if (!ctx) return;
-  cudaSetDevice(ctx->device);
+  DeviceGuard guard(ctx->device);
   cudaFree(ctx->d_bkf);
   cudaFree(ctx->d_bkw);
   cudaFree(ctx->d_wtw);
@@ -1146,7 +996,7 @@ void tfb_ctx_destroy(tfb_ctx* ctx) {
 int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_device, void* stream) {
   if (!ctx || !bk || !ksk) return TFB_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
-  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  TFB_ENTER(ctx);
   const int n = ctx->p.n;
   const size_t bk_words = (size_t)n * BK_ROWS * 2 * RING_N;
   const size_t ksk_words = (size_t)RING_N * KS_T * (n + 1);
@@ -1299,7 +1149,7 @@ int tfb_gate_launch(tfb_ctx* ctx, void* pool, const uint8_t* kinds, const int32_
   if (rc) return rc;
   if (!pool || !kinds || !xr || !yr || !out_rows) return TFB_ERR_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
-  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  TFB_ENTER(ctx);
   if ((rc = ensure_ext(ctx, k))) return rc;
   if ((rc = launch_blind_rotate(ctx, pool, ROW_STRIDE, kinds, xr, yr, ctx->d_ext, k, st))) return rc;
   return launch_key_switch(ctx, ctx->d_ext, pool, ROW_STRIDE, out_rows, k, st);
@@ -1310,7 +1160,7 @@ int tfb_debug_blind_rotate(tfb_ctx* ctx, const void* pool, const uint8_t* kinds,
   int rc = check_launch_args(ctx, k);
   if (rc) return rc;
   if (!pool || !kinds || !xr || !yr || !ext) return TFB_ERR_INVALID;
-  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  TFB_ENTER(ctx);
   return launch_blind_rotate(ctx, pool, ROW_STRIDE, kinds, xr, yr, ext, k, (cudaStream_t)stream);
 }
 
@@ -1319,7 +1169,7 @@ int tfb_debug_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, const in
   int rc = check_launch_args(ctx, k);
   if (rc) return rc;
   if (!pool || !ext || !out_rows) return TFB_ERR_INVALID;
-  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  TFB_ENTER(ctx);
   return launch_key_switch(ctx, ext, pool, ROW_STRIDE, out_rows, k, (cudaStream_t)stream);
 }
 
@@ -1328,7 +1178,7 @@ int tfb_gate_launch_host(tfb_ctx* ctx, const uint32_t* x, const uint32_t* y, con
   int rc = check_launch_args(ctx, k);
   if (rc) return rc;
   if (!x || !y || !kinds || !out) return TFB_ERR_INVALID;
-  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  TFB_ENTER(ctx);
   if (k > ctx->host_cap) {
     cudaFree(ctx->d_hx);
     cudaFree(ctx->d_hkinds);
@@ -1394,7 +1244,7 @@ int tfb_gate_launch_host(tfb_ctx* ctx, const uint32_t* x, const uint32_t* y, con
 int tfb_rows_negate(tfb_ctx* ctx, void* pool, const int32_t* in_rows, const int32_t* out_rows, int64_t k,
                     void* stream) {
   if (!ctx || !pool || !in_rows || !out_rows || k < 1) return TFB_ERR_INVALID;
-  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  TFB_ENTER(ctx);
   k_rows_negate<<<(unsigned)k, 128, 0, (cudaStream_t)stream>>>((uint32_t*)pool, in_rows, out_rows);
   ctx->launches += 1;
   TFB_CUDA(ctx, cudaGetLastError());
@@ -1404,7 +1254,7 @@ int tfb_rows_negate(tfb_ctx* ctx, void* pool, const int32_t* in_rows, const int3
 int tfb_rows_phase(tfb_ctx* ctx, const void* pool, const int32_t* rows, const uint32_t* key_bits,
                    uint32_t* phase, int64_t k, void* stream) {
   if (!ctx || !pool || !rows || !key_bits || !phase || k < 1) return TFB_ERR_INVALID;
-  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  TFB_ENTER(ctx);
   k_rows_phase<<<(unsigned)k, 128, 0, (cudaStream_t)stream>>>((const uint32_t*)pool, rows, key_bits, phase,
                                                              ctx->p.n);
   ctx->launches += 1;
@@ -1415,7 +1265,7 @@ int tfb_rows_phase(tfb_ctx* ctx, const void* pool, const int32_t* rows, const ui
 int tfb_debug_spectral_key(tfb_ctx* ctx, int32_t i, double* out) {
   if (!ctx || !out || i < 0 || i >= ctx->p.n) return TFB_ERR_INVALID;
   if (!ctx->keys_loaded) return TFB_ERR_STATE;
-  TFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  TFB_ENTER(ctx);
   const size_t per_i = (size_t)2 * STAGE_CD;
   std::vector<cd> h(per_i);
   TFB_CUDA(ctx, cudaMemcpy(h.data(), ctx->d_bkf + (size_t)i * per_i, per_i * sizeof(cd), cudaMemcpyDeviceToHost));
@@ -1443,7 +1293,8 @@ int tfb_debug_pick_kernel(int64_t k, int sms, int64_t* body_gates) {
 int64_t tfb_kernel_launches(const tfb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int tfb_measure_peaks(int device, double* fp64_tflops, double* int32_tops) {
-  if (cudaSetDevice(device) != cudaSuccess) return TFB_ERR_CUDA;
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) return TFB_ERR_CUDA;
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return TFB_ERR_CUDA;
   const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 1 << 16;

@@ -692,15 +692,18 @@ class B200Engine(GateEngine):
         return self._torch.from_numpy(np.ascontiguousarray(arr, dtype=dtype)).to(self.device)
 
     # -- evaluation -------------------------------------------------------------------------
+    EVAL_CHUNK = 1 << 18  # gates per tfb_gate_launch: bounds the library's extracted-sample scratch at 1.1 GB
+
     def _evaluate(self, kind_ids, x_rows, y_rows, out_rows) -> None:
         self._flush()
         k = len(kind_ids)
         idx = self._dev(np.concatenate([x_rows, y_rows, out_rows]), np.int32)
         kinds = self._dev(kind_ids, np.uint8)
         base, step = idx.data_ptr(), 4 * k
-        with self._torch.cuda.device(self.device):
-            self._ctx.call("tfb_gate_launch", self._pool_t.data_ptr(), kinds.data_ptr(), base, base + step,
-                           base + 2 * step, k, self._stream())
+        for lo in range(0, k, self.EVAL_CHUNK):  # gates of a launch are independent: chunking is unobservable
+            kc = min(self.EVAL_CHUNK, k - lo)
+            self._ctx.call("tfb_gate_launch", self._pool_t.data_ptr(), kinds.data_ptr() + lo, base + 4 * lo,
+                           base + step + 4 * lo, base + 2 * step + 4 * lo, kc, self._stream())
 
     def _refresh(self, in_rows, out_rows) -> None:
         self._submit(np.full(len(in_rows), IDENTITY_KIND_ID, np.uint8), in_rows, in_rows, out_rows)

@@ -151,8 +151,11 @@ def _take_records(c: _Cursor, count: int, params: LweParams | None):
         raise FormatError(f"bad torus precision {w}")
     if params is not None and (w != params.w or m != params.m):
         raise FormatError("sample dimensions do not match the engine parameters")
+    need = (8 * m + 21) * count  # u8 w, u32 m, m x u64 mask, u64 body, f64 bound per record
+    if need > len(c.view) - c.at:  # before the dtype exists: m comes from an untrusted header
+        raise FormatError("truncated payload")
     dt = _record_dtype(m)
-    rec = np.frombuffer(c.take(dt.itemsize * count), dtype=dt)
+    rec = np.frombuffer(c.take(need), dtype=dt)
     if np.any(rec["w"] != w) or np.any(rec["m"] != m):
         raise FormatError("sample dimensions do not match the engine parameters" if params is not None
                           else "mixed sample dimensions")
@@ -161,7 +164,7 @@ def _take_records(c: _Cursor, count: int, params: LweParams | None):
         raise FormatError("mask word exceeds torus modulus")
     words = np.empty((count, m + 1), dtype=word_dtype(w))
     words[:, :-1] = rec["a"]
-    words[:, -1] = rec["b"] & np.uint64(limit)
+    words[:, -1] = rec["b"] & np.uint64(limit)  # the reference reduces the body word too (LweSample masks b)
     return words, rec["bound"].copy(), w
 
 

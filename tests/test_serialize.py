@@ -89,3 +89,14 @@ def test_evaluation_keys_roundtrip(eval_keys):
     assert np.array_equal(back.ring_key, eval_keys.ring_key)
     with pytest.raises(FormatError):
         load_eval_keys(blob[:-4])
+
+
+def test_untrusted_sample_header_cannot_size_an_allocation():
+    """A sample payload announcing a huge m must fail as a truncated payload (FormatError), not while numpy
+    builds a record type from the header (reference contract: encirc/serialize.py:46-58)."""
+    import struct
+
+    for m in (0xFFFFFFFF, 0x10000000, 501):
+        blob = b"ENC\x01S" + struct.pack("<BI", 32, m) + b"\x00" * 64
+        with pytest.raises(FormatError):
+            load_sample(blob)
