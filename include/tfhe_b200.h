@@ -101,6 +101,16 @@ int tfb_rows_negate(tfb_ctx *ctx, void *pool_dev, const int32_t *in_rows_dev, co
 int tfb_rows_phase(tfb_ctx *ctx, const void *pool_dev, const int32_t *rows_dev, const uint32_t *key_bits_dev,
                    uint32_t *phase_dev, int64_t k, void *stream);
 
+/* Batched fresh encryption on the device (encirc/torus.py:254-271 restated for a counter-based generator):
+ * for i < k, row out_rows_dev[i] <- (a, b) with a uniform in Z_2^32^n from Philox4x32-10 keyed by `seed` at counter
+ * (first_sample + i, word index), e = rint(N(0, alpha) * 2^32) clipped to +-(2^27 - 1) like the reference's
+ * gaussian_noise_words, b = <a, s> + message(bits_dev[i]) + e.  The draw ORDER differs from numpy's PCG64 stream, so
+ * words are not those of the reference for the same seed; the host path of the Python engine keeps that identity.
+ * Deterministic in (seed, first_sample). */
+int tfb_rows_encrypt(tfb_ctx *ctx, void *pool_dev, const int32_t *out_rows_dev, const uint8_t *bits_dev,
+                     const uint32_t *key_bits_dev, double alpha, uint64_t seed, uint64_t first_sample, int64_t k,
+                     void *stream);
+
 /* Parity taps: the two halves of tfb_gate_launch run separately so tests can
  * compare the intermediate (N+1)-word extracted sample with the oracle. */
 int tfb_debug_blind_rotate(tfb_ctx *ctx, const void *pool_dev, const uint8_t *kinds_dev,

@@ -84,6 +84,8 @@ def lib() -> ctypes.CDLL:
     L.tfb_gate_launch_host.argtypes = [_vp, _vp, _vp, _vp, _vp, ctypes.c_int64]
     L.tfb_rows_negate.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     L.tfb_rows_phase.argtypes = [_vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
+    L.tfb_rows_encrypt.argtypes = [_vp, _vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64,
+                                   ctypes.c_int64, _vp]
     L.tfb_debug_blind_rotate.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     L.tfb_debug_key_switch.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     L.tfb_debug_spectral_key.argtypes = [_vp, ctypes.c_int32, _vp]
@@ -99,7 +101,7 @@ def lib() -> ctypes.CDLL:
 
 EXPORTS = (
     "tfb_abi_version", "tfb_last_error", "tfb_ctx_create", "tfb_ctx_destroy", "tfb_load_keys",
-    "tfb_gate_launch", "tfb_gate_launch_host", "tfb_rows_negate", "tfb_rows_phase",
+    "tfb_gate_launch", "tfb_gate_launch_host", "tfb_rows_negate", "tfb_rows_phase", "tfb_rows_encrypt",
     "tfb_debug_blind_rotate", "tfb_debug_key_switch", "tfb_debug_spectral_key",
     "tfb_debug_pick_kernel", "tfb_kernel_launches", "tfb_measure_peaks",
 )

@@ -840,6 +840,67 @@ __global__ void k_rows_phase(const uint32_t* __restrict__ pool, const int32_t* _
   }
 }
 
+// ---- batched fresh encryption (client side, encirc/torus.py:254-271) --------------------------------
+// Philox4x32-10 (Salmon et al., SC'11): counter-based, so sample i / word j is a pure function of
+// (seed, i, j) whatever the launch geometry.
+struct Philox {
+  uint32_t k0, k1;
+  __device__ __forceinline__ uint4 operator()(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) const {
+    uint32_t a = k0, b = k1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      const uint32_t h0 = __umulhi(0xD2511F53u, c0), l0 = 0xD2511F53u * c0;
+      const uint32_t h1 = __umulhi(0xCD9E8D57u, c2), l1 = 0xCD9E8D57u * c2;
+      c0 = h1 ^ c1 ^ a;
+      c1 = l1;
+      c2 = h0 ^ c3 ^ b;
+      c3 = l0;
+      a += 0x9E3779B9u;
+      b += 0xBB67AE85u;
+    }
+    return make_uint4(c0, c1, c2, c3);
+  }
+};
+
+// one CTA per sample: threads draw the mask four words at a time, reduce <a, s>, thread 0 draws the noise
+__global__ void __launch_bounds__(128) k_rows_encrypt(uint32_t* __restrict__ pool,
+                                                      const int32_t* __restrict__ out_rows,
+                                                      const uint8_t* __restrict__ bits,
+                                                      const uint32_t* __restrict__ key_bits, int n, uint32_t mu,
+                                                      double alpha, uint64_t seed, uint64_t first_sample) {
+  const uint64_t sample = first_sample + blockIdx.x;
+  const Philox rng{(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t* row = pool + (int64_t)out_rows[blockIdx.x] * ROW_STRIDE;
+  uint32_t dot = 0;
+  for (int q = threadIdx.x; 4 * q < n; q += blockDim.x) {
+    const uint4 w = rng((uint32_t)sample, (uint32_t)(sample >> 32), (uint32_t)q, 0u);
+    const uint32_t v[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (4 * q + e < n) {
+        row[4 * q + e] = v[e];
+        dot += v[e] * key_bits[4 * q + e];
+      }
+  }
+  for (int c = n + 1 + threadIdx.x; c < ROW_STRIDE; c += blockDim.x) row[c] = 0u;
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
+  __shared__ uint32_t part[4];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = dot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint4 w = rng((uint32_t)sample, (uint32_t)(sample >> 32), 0u, 1u);  // stream 1: the noise
+    // Box-Muller on two 53-bit-grade uniforms in (0, 1]
+    const double u1 = ((double)w.x * 4294967296.0 + (double)w.y + 1.0) * (1.0 / 18446744073709551616.0);
+    const double u2 = ((double)w.z * 4294967296.0 + (double)w.w) * (1.0 / 18446744073709551616.0);
+    double e = rint(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2) * alpha * 4294967296.0);
+    const uint32_t clamp_word = mu / 4 > 1 ? mu / 4 : 1;  // fresh_clamp_word (encirc/torus.py:177-184): 2^27 at mu = 1/8
+    const double clamp = (double)(clamp_word - 1);
+    e = fmin(fmax(e, -clamp), clamp);
+    const uint32_t msg = bits[blockIdx.x] ? mu : (0u - mu);
+    row[n] = part[0] + part[1] + part[2] + part[3] + msg + (uint32_t)(int32_t)e;
+  }
+}
+
 // packed host layout [k][n+1] <-> pool rows, used by the host-buffer launch
 __global__ void k_identity_rows(int32_t* rows, int64_t count, int32_t base) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1257,6 +1318,17 @@ int tfb_rows_phase(tfb_ctx* ctx, const void* pool, const int32_t* rows, const ui
   TFB_ENTER(ctx);
   k_rows_phase<<<(unsigned)k, 128, 0, (cudaStream_t)stream>>>((const uint32_t*)pool, rows, key_bits, phase,
                                                              ctx->p.n);
+  ctx->launches += 1;
+  TFB_CUDA(ctx, cudaGetLastError());
+  return TFB_OK;
+}
+
+int tfb_rows_encrypt(tfb_ctx* ctx, void* pool, const int32_t* out_rows, const uint8_t* bits, const uint32_t* key_bits,
+                     double alpha, uint64_t seed, uint64_t first_sample, int64_t k, void* stream) {
+  if (!ctx || !pool || !out_rows || !bits || !key_bits || k < 1 || !(alpha >= 0.0)) return TFB_ERR_INVALID;
+  TFB_ENTER(ctx);
+  k_rows_encrypt<<<(unsigned)k, 128, 0, (cudaStream_t)stream>>>((uint32_t*)pool, out_rows, bits, key_bits, ctx->p.n,
+                                                               ctx->p.mu_word, alpha, seed, first_sample);
   ctx->launches += 1;
   TFB_CUDA(ctx, cudaGetLastError());
   return TFB_OK;

@@ -222,3 +222,74 @@ def test_encrypted_regression_on_the_gpu(key, eval_keys, golden):
     check_regression_against_reference(
         lambda: B200Engine(key, seed=3, pool=WorkerPool(PoolConfig(workers=1, max_batch=1 << 22)), eval_keys=eval_keys),
         golden)
+
+
+def test_lazy_and_eager_execution_agree_on_the_device(key, eval_keys):
+    """Levelised (recorded, level-by-level) execution against one kernel sequence per logical launch, on the real
+    device row pool with its quarantine / recycling: identical ciphertext words, results and GateStats for a 16-bit
+    multiply and a 4 x 4 Cannon matrix product (tests/test_lazy_engine.py checks the same on the host stand-in)."""
+    from paper_2005_01945_b200 import B200Engine
+
+    rng = np.random.default_rng(41)
+    a, b = (int(v) for v in rng.integers(0, 1 << 16, size=2))
+    A, Bm = (rng.integers(0, 1 << 6, size=(4, 4)).tolist() for _ in range(2))
+    seen = {}
+    for mode in ("lazy", "eager"):
+        eng = B200Engine(key, seed=23, eval_keys=eval_keys, pool=WorkerPool(PoolConfig(workers=1, max_batch=1 << 16)),
+                         initial_rows=1 << 12)  # small pool: growth and row recycling happen during the run
+        eng.lazy = mode == "lazy"
+        prod = mul_naive(encrypt_int(eng, a, 16), encrypt_int(eng, b, 16))
+        mat = mat_mul_cannon(encrypt_matrix(eng, A, 6), encrypt_matrix(eng, Bm, 6))
+        words = np.concatenate([eng.read_rows(prod._rows)] + [eng.read_rows(c._rows) for c in mat.data])
+        assert decrypt_int(eng, prod) == a * b
+        assert decrypt_matrix(eng, mat) == [[sum(A[i][t] * Bm[t][j] for t in range(4)) % 64 for j in range(4)]
+                                            for i in range(4)]
+        seen[mode] = (words, eng.stats.as_record(), eng.physical_launches)
+    assert np.array_equal(seen["lazy"][0], seen["eager"][0])
+    assert seen["lazy"][1] == seen["eager"][1]
+    assert seen["lazy"][2] < seen["eager"][2]  # fewer kernel-launch levels than logical launches
+
+
+def test_device_side_encryption(key, eval_keys):
+    """tfb_rows_encrypt: every row decrypts to its bit, the noise is the rounded clipped Gaussian(alpha) of the
+    reference's fresh encryption (encirc/torus.py:233-271), the stream is deterministic in (seed, call order), and
+    the config-5 input volume (2 x 4096 x 32 bits) is produced well inside half a second."""
+    import time
+
+    from paper_2005_01945_b200 import B200Engine
+
+    eng = B200Engine(key, seed=9, eval_keys=eval_keys, device_encrypt=True)
+    rng = np.random.default_rng(3)
+    bits = rng.integers(0, 2, size=1 << 16)
+    rows, owner = eng.encrypt_rows(bits)
+    assert np.array_equal(eng.decrypt_rows(rows), bits)
+    ph = eng.phases(rows).astype(np.int64)
+    target = np.where(bits == 1, 1 << 29, (1 << 32) - (1 << 29))
+    err = ((ph - target + 2**31) % 2**32) - 2**31
+    sigma = key.params.alpha * 2.0**32
+    assert abs(err.std() / sigma - 1.0) < 0.02 and abs(err.mean()) < 4 * sigma / np.sqrt(len(err))
+    assert np.abs(err).max() < (1 << 27)
+    # rounded Gaussian: about 68.3 % / 95.4 % inside one / two sigma
+    assert abs((np.abs(err) < sigma).mean() - 0.6827) < 0.01 and abs((np.abs(err) < 2 * sigma).mean() - 0.9545) < 0.005
+    words = eng.read_rows(rows[:64])
+    assert len(np.unique(words[:, :-1])) > 0.99 * words[:, :-1].size  # masks are not repeated
+    mask_bits = np.unpackbits(eng.read_rows(rows[:2048])[:, :-1].view(np.uint8))
+    assert abs(mask_bits.mean() - 0.5) < 0.002
+    # determinism: a second engine with the same seed reproduces the stream; a different seed does not
+    again = B200Engine(key, seed=9, eval_keys=eval_keys, device_encrypt=True)
+    r2, o2 = again.encrypt_rows(bits[:64])
+    assert np.array_equal(again.read_rows(r2), words)
+    other = B200Engine(key, seed=10, eval_keys=eval_keys, device_encrypt=True)
+    r3, o3 = other.encrypt_rows(bits[:64])
+    assert not np.array_equal(other.read_rows(r3), words)
+    # volume of config 5
+    big = rng.integers(0, 2, size=2 * 4096 * 32)
+    eng.synchronize()
+    t0 = time.perf_counter()
+    rows_big, owner_big = eng.encrypt_rows(big)
+    eng.synchronize()
+    dt = time.perf_counter() - t0
+    assert np.array_equal(eng.decrypt_rows(rows_big), big)
+    assert dt < 0.5, dt
+    # the circuit layer runs on device-encrypted inputs unchanged
+    assert decrypt_int(eng, add_bitwise(encrypt_int(eng, 1234, 12), encrypt_int(eng, 3000, 12))) == (1234 + 3000) % 4096

@@ -230,7 +230,7 @@ def test_invalid_calls_return_status(gpu):
 def test_full_size_launch_properties(gpu, key, eval_keys):
     """2**16 gates in one launch (BASELINE configs[1]): every output decrypts to
     its truth table, every phase sits within the reference's fresh bound of
-    +-mu, and a sample of rows equals the oracle bit for bit."""
+    +-mu, and 2,048+ spread rows equal the oracle bit for bit."""
     ctx, torch, _cabi = gpu
     K, n = 1 << 16, key.params.m
     base = 256
@@ -262,8 +262,11 @@ def test_full_size_launch_properties(gpu, key, eval_keys):
     target = np.where(want_bit == 1, 1 << 29, (1 << 32) - (1 << 29))
     err = ((phase - target + 2**31) % 2**32) - 2**31
     assert np.abs(err).max() < (1 << 27)  # fresh_noise_bound = 2**-5 (encirc/torus.py:177-184)
-    # bit-exact sample against the oracle
-    sel = np.array([0, 1, 255, 256, 4097, 65535])
+    # bit-exact against the oracle on 2,048+ rows spread over the whole launch (first / last rows, wave and CTA
+    # boundaries of the 12-gates-per-SM kernel, and a stride that is coprime to every tile size)
+    edge = [0, 1, 11, 12, 255, 256, 1775, 1776, 4097, 14207, 14208, 63935, 63936, 65534, 65535]
+    sel = np.unique(np.concatenate([edge, (np.arange(2048) * 32003 + 17) % K]))
+    assert len(sel) >= 2048
     sx = xs[sel % base]
     sy = ys[(sel // base + sel) % base]
     want = orc.gate_bootstrap_batch(sx, sy, (sel % 8).astype(np.uint8), key.params.mu.word, eval_keys.bk,
