@@ -449,16 +449,31 @@ struct WarpRing {
     }
     ++chunk;
   }
-  __device__ __forceinline__ void skip(int) {
-#pragma unroll 1
-    for (int j = 0; j < 4; ++j) {
-      acquire_chunk(0, 0, 0);
-      release();
-    }
-  }
 };
 
+// Turn protocol (TFB_K1D_TURNS): the three warps that share a scheduler take the MAC stage of a CMux in
+// a fixed rotation, handing the turn on with named barriers (bar.arrive by the warp that leaves, bar.sync
+// by the next: a hardware wait, no issue slots).  Left alone, the round-robin scheduler convoys the
+// warps: all three want the FP64 pipe in the same cycles (math-pipe-throttle / not-selected stalls) and
+// then sit in their shared-memory phases together.  One fixed hand-over per stage pins them a third of a
+// stage apart -- one in its MAC (key loads, tensor-memory traffic), two in transforms: 68.3 -> 64.4 ms
+// per 14,208 gates.  What was measured and lost (turns around the FP64 bursts, around both, a
+// first-come-first-served lock instead of the rotation) is in profiles/README.md.
+#ifndef TFB_K1D_TURNS
+#define TFB_K1D_TURNS 1
+#endif
 struct DevWarp {
+  int turn_wait = 0, turn_next = 0;  // named-barrier ids (0: no protocol, e.g. the key-setup kernel)
+  __device__ __forceinline__ void turn_enter() const {
+    if (TFB_K1D_TURNS && turn_wait) asm volatile("bar.sync %0, 64;" ::"r"(turn_wait) : "memory");
+  }
+  __device__ __forceinline__ void turn_leave() const {
+    if (TFB_K1D_TURNS && turn_next) asm volatile("bar.arrive %0, 64;" ::"r"(turn_next) : "memory");
+  }
+  __device__ __forceinline__ void turn_pass() const {  // take the turn and hand it on at once
+    turn_enter();
+    turn_leave();
+  }
   __device__ __forceinline__ void operator()() const { __syncwarp(); }
   __device__ __forceinline__ cd xchg16(cd v) const {
     return cd{__shfl_xor_sync(0xffffffffu, v.re, 16), __shfl_xor_sync(0xffffffffu, v.im, 16)};
@@ -652,6 +667,18 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
   const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
   uint32_t* dst = want < k ? ext + g * EXT_STRIDE : nullptr;  // null: no extract
   DevWarp w;
+#if TFB_K1D_TURNS
+  {
+    // rotation over the warps {s, s + 4, s + 8} of scheduler s = wid % 4 (grouping {3 s, 3 s + 1, 3 s + 2} measured
+    // 8 % slower: warp w runs on scheduler w % 4): position r = wid / 4 waits on the barrier its predecessor
+    // arrives on; the last position pre-arrives once so that position 0 starts
+    static_assert(K1D_WARPS == 12, "the turn rotation is laid out for three warps per scheduler");
+    const int sch = wid & 3, pos = wid >> 2;
+    w.turn_wait = 1 + 3 * sch + (pos + 2) % 3;
+    w.turn_next = 1 + 3 * sch + pos;
+    if (pos == 2) w.turn_leave();
+  }
+#endif
 #if TFB_K1D_TMEM
   TmemWPark park{tmem_base + ((((uint32_t)wid & 3u) * 32u) << 16) + ((uint32_t)wid >> 2) * K1D_TMEM_SLICE};
 #else

@@ -33,6 +33,9 @@
 namespace tfb {
 
 constexpr int WARP_T = 32;  // lanes per ciphertext
+// Turn protocol (W::turn_enter / turn_leave / turn_pass): the warps that share a scheduler take the MAC
+// stage of a CMux in a fixed rotation, which keeps them a third of a stage apart (see DevWarp in
+// tfhe_b200.cu for why).  Measured placements are listed in profiles/README.md.
 constexpr int WPTS = 16;    // points per lane
 
 // Per-lane twiddles (t = lane, r = t & 15, h = t >> 4).  Lane h = 1 keeps its pass-1 outputs
@@ -65,10 +68,10 @@ inline void fill_warp_twiddles(WarpTwiddles* tw, Real (*cosf_)(Real), Real (*sin
   }
 }
 
-// exp(i pi m / 32), m in [0, 16]: register part of the twist; exp(i pi j / 16) = twist16(2 j).
-// On the device the table sits in the constant bank, so that FP64 instructions take these
-// factors as c[][] operands: as literals the compiler hoists them out of the blind-rotation
-// loop into ~70 registers and then spills them.
+// cos(pi m / 32), m in [0, 16]: every compile-time twiddle of the 16-point transforms is a point of this
+// first quadrant up to symmetry.  On the device the table sits in the constant bank, so that FP64
+// instructions take these factors as c[][] operands (sign flips ride in the operand modifiers): as
+// literals the compiler hoists them out of the blind-rotation loop into ~70 registers and spills them.
 #define TFB_TWIST16_VALUES                                                                                   \
   {1.0, 0.9951847266721969, 0.9807852804032304, 0.9569403357322088, 0.9238795325112867, 0.881921264348355,  \
    0.8314696123025452, 0.773010453362737, 0.7071067811865476, 0.6343932841636455, 0.5555702330196023,       \
@@ -76,47 +79,72 @@ inline void fill_warp_twiddles(WarpTwiddles* tw, Real (*cosf_)(Real), Real (*sin
 #if defined(__CUDACC__)
 __constant__ double kTwist16Dev[17] = TFB_TWIST16_VALUES;
 #endif
-TFB_HD cd twist16(int m) {
+TFB_HD double quadrant_cos(int m) {  // cos(pi m / 32), 0 <= m <= 16
 #if defined(__CUDA_ARCH__)
-  return cd{kTwist16Dev[m], kTwist16Dev[16 - m]};
+  return kTwist16Dev[m];
 #else
   const double C[17] = TFB_TWIST16_VALUES;
-  return cd{C[m], C[16 - m]};
+  return C[m];
 #endif
 }
+TFB_HD double cospi32(int j) {  // cos(pi j / 32), any integer j (a compile-time constant after unrolling)
+  j &= 63;
+  if (j > 32) j = 64 - j;
+  return j <= 16 ? quadrant_cos(j) : -quadrant_cos(32 - j);
+}
+TFB_HD cd expi32(int j) { return cd{cospi32(j), cospi32(j - 16)}; }  // exp(i pi j / 32)
+TFB_HD cd twist16(int m) { return expi32(m); }                       // register part of the negacyclic twist
 
-// ---- 16-point DFT in registers: X[k] = sum_m x[m] exp(SIGN 2 pi i m k / 16), natural order ----
+// ---- 16-point DFTs in registers, FMA form -------------------------------------------------------
+// K1d is limited by the FP64 pipe together with latency, so every twiddle multiplication that feeds a
+// butterfly is folded into it:  (a + w b, a - w b)  costs six FMA-class instructions (four for the sum,
+// then a - w b = 2 a - (a + w b)) instead of a complex multiplication plus two complex additions (eight).
+TFB_HD void bfly(cd a, cd b, cd w, cd& p, cd& m) {  // p = a + w b, m = a - w b
+  p.re = fma(-w.im, b.im, fma(w.re, b.re, a.re));
+  p.im = fma(w.im, b.re, fma(w.re, b.im, a.im));
+  m.re = fma(2.0, a.re, -p.re);
+  m.im = fma(2.0, a.im, -p.im);
+}
 template <int SIGN>
-TFB_HD void dft4(cd& z0, cd& z1, cd& z2, cd& z3) {
+TFB_HD void dft4(cd& z0, cd& z1, cd& z2, cd& z3) {  // y_k = sum_j z_j i^(SIGN j k), in place
   const cd t0 = cadd(z0, z2), t1 = csub(z0, z2), t2 = cadd(z1, z3), t3 = mul_i<SIGN>(csub(z1, z3));
   z0 = cadd(t0, t2);
   z1 = cadd(t1, t3);
   z2 = csub(t0, t2);
   z3 = csub(t1, t3);
 }
-
+// the same on (z0, w1 z1, w2 z2, w3 z3): 24 instructions instead of 12 + 16.  W2I: w2 = i^SIGN (free).
+template <int SIGN, bool W2I = false>
+TFB_HD void dft4_tw(cd& z0, cd& z1, cd& z2, cd& z3, cd w1, cd w2, cd w3) {
+  cd t0, t1, t2, t3;
+  if (W2I) {
+    const cd v = mul_i<SIGN>(z2);
+    t0 = cadd(z0, v);
+    t1 = csub(z0, v);
+  } else {
+    bfly(z0, z2, w2, t0, t1);
+  }
+  bfly(cmul(z1, w1), z3, w3, t2, t3);
+  t3 = mul_i<SIGN>(t3);
+  z0 = cadd(t0, t2);
+  z1 = cadd(t1, t3);
+  z2 = csub(t0, t2);
+  z3 = csub(t1, t3);
+}
+// ... and with a twiddle on z0 as well (28 instructions)
 template <int SIGN>
-TFB_HD cd mul_w16(cd v, int e) {  // v * exp(SIGN 2 pi i e / 16), e a compile-time constant after unrolling
-  const double c1 = 0.9238795325112867, s1 = 0.3826834323650898, h = 0.7071067811865476;
-  const double CO[10] = {1.0, c1, h, s1, 0.0, -s1, -h, -c1, -1.0, -c1};
-  const double SI[10] = {0.0, s1, h, c1, 1.0, c1, h, s1, 0.0, -s1};
-  if (e == 0) return v;
-  if (e == 4) return mul_i<SIGN>(v);
-  return cmul(v, cd{CO[e], SIGN * SI[e]});
+TFB_HD void dft4_tw4(cd& z0, cd& z1, cd& z2, cd& z3, cd w0, cd w1, cd w2, cd w3) {
+  cd t0, t1, t2, t3;
+  bfly(cmul(z0, w0), z2, w2, t0, t1);
+  bfly(cmul(z1, w1), z3, w3, t2, t3);
+  t3 = mul_i<SIGN>(t3);
+  z0 = cadd(t0, t2);
+  z1 = cadd(t1, t3);
+  z2 = csub(t0, t2);
+  z3 = csub(t1, t3);
 }
 
-template <int SIGN>
-TFB_HD void dft16(cd* x) {
-#pragma unroll
-  for (int a = 0; a < 4; ++a) dft4<SIGN>(x[a], x[a + 4], x[a + 8], x[a + 12]);
-    // x[a + 4 k0] = y_a[k0]; twiddle w16^{a k0}
-#pragma unroll
-  for (int a = 1; a < 4; ++a)
-#pragma unroll
-    for (int k0 = 1; k0 < 4; ++k0) x[a + 4 * k0] = mul_w16<SIGN>(x[a + 4 * k0], a * k0);
-#pragma unroll
-  for (int k0 = 0; k0 < 4; ++k0) dft4<SIGN>(x[4 * k0], x[4 * k0 + 1], x[4 * k0 + 2], x[4 * k0 + 3]);
-    // x[k1 + 4 k0] = X[k0 + 4 k1]: transpose to natural order (register renaming)
+TFB_HD void transpose4x4(cd* x) {  // x[i + 4 j] <-> x[j + 4 i]: register renaming
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -125,6 +153,38 @@ TFB_HD void dft16(cd* x) {
       x[i + 4 * j] = x[j + 4 * i];
       x[j + 4 * i] = tmp;
     }
+}
+
+// second radix-4 layer of a 16-point DFT with the mid twiddles w16^(SIGN a k0) folded in
+// (in: x[a + 4 k0] = y_a[k0]; out: x[4 k0 + k1] = X[k0 + 4 k1]), 86 instead of 96 instructions
+template <int SIGN>
+TFB_HD void dft16_layer_b(cd* x) {
+  dft4<SIGN>(x[0], x[1], x[2], x[3]);
+  dft4_tw<SIGN>(x[4], x[5], x[6], x[7], expi32(SIGN * 4), expi32(SIGN * 8), expi32(SIGN * 12));
+  dft4_tw<SIGN, true>(x[8], x[9], x[10], x[11], expi32(SIGN * 8), expi32(SIGN * 16), expi32(SIGN * 24));
+  dft4_tw<SIGN>(x[12], x[13], x[14], x[15], expi32(SIGN * 12), expi32(SIGN * 24), expi32(SIGN * 36));
+}
+
+// X[k] = sum_m x[m] exp(SIGN 2 pi i m k / 16), natural order in and out
+template <int SIGN>
+TFB_HD void dft16(cd* x) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a) dft4<SIGN>(x[a], x[a + 4], x[a + 8], x[a + 12]);
+  dft16_layer_b<SIGN>(x);
+  transpose4x4(x);
+}
+
+// X[k] = sum_m (x[m] exp(i pi m / 32)) exp(2 pi i m k / 16): the register part of the negacyclic twist folded
+// into both radix-4 layers (inner twists exp(i pi 4 b / 32) on the inputs of layer A, exp(i pi a (1 + 4 k0) / 32)
+// on those of layer B): 192 instead of 60 + 160 instructions
+TFB_HD void dft16_twisted(cd* x) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a) dft4_tw<1>(x[a], x[a + 4], x[a + 8], x[a + 12], expi32(4), expi32(8), expi32(12));
+#pragma unroll
+  for (int k0 = 0; k0 < 4; ++k0)
+    dft4_tw<1>(x[4 * k0], x[4 * k0 + 1], x[4 * k0 + 2], x[4 * k0 + 3], expi32(1 + 4 * k0), expi32(2 * (1 + 4 * k0)),
+               expi32(3 * (1 + 4 * k0)));
+  transpose4x4(x);
 }
 
 // Exchange buffer slot of U[r][k1][b]: rows of 32 values padded to 33, so that both sides
@@ -181,10 +241,12 @@ TFB_HD void wexchange(cd* x, int t, void* buf, W& w) {
   }
 }
 
-// The 16 pass-1 twiddles of a lane in register order (0..7 from sa, 8..15 from sb, each times
-// g, g^2, ...) and the radix-2 twiddle c.  Built once per lane; a twiddle provider hands them
-// to the transforms in chunks of four:
-//   issue4(kb, chunk) / settle4(chunk, w): twiddles kb .. kb+3;   issue_c / settle_c: the radix-2 twiddle
+// The 16 pass-1 twiddles of a lane (natural index k: 0..7 from sa, 8..15 from sb, each times g, g^2, ...)
+// and the radix-2 twiddle c.  Built once per lane and stored in GROUP order, w[4 a + b] = twiddle of
+// register a + 4 b: group a = registers (a, a+4, a+8, a+12) is what one radix-4 butterfly of the inverse
+// and two radix-2 butterflies of the forward transform consume.  A twiddle provider hands them to the
+// transforms one group at a time:
+//   issue4(4 a, chunk) / settle4(chunk, w): group a;   issue_c / settle_c: the radix-2 twiddle
 // (the B200 kernel keeps the table in tensor memory: rebuilding the chain inside every
 // transform costs 56 FP64 instructions per transform on the pipe that limits K1d).
 struct LaneTwiddles {
@@ -195,9 +257,9 @@ TFB_HD void build_lane_twiddles(const WarpTwiddles* tw, int t, LaneTwiddles* out
   const cd g = tw->g[t];
   cd wa = tw->sa[t], wb = tw->sb[t];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    out->w[j] = wa;
-    out->w[8 + j] = wb;
+  for (int j = 0; j < 8; ++j) {  // natural registers j and 8 + j
+    out->w[4 * (j & 3) + (j >> 2)] = wa;
+    out->w[4 * (j & 3) + 2 + (j >> 2)] = wb;
     wa = cmul(wa, g);
     wb = cmul(wb, g);
   }
@@ -235,7 +297,8 @@ TFB_HD void wflip_odd(cd* x, uint32_t sgn) {
 }
 
 // W: warp primitives -- operator()() = warp barrier with memory ordering, xchg16(v) = the
-// value lane (t ^ 16) passed.
+// value lane (t ^ 16) passed, turn_enter() / turn_leave() bracket the MAC stage (the B200 kernel
+// rotates a turn between the warps of a scheduler there, see DevWarp; no-ops elsewhere).
 //
 // Forward negacyclic transform, unnormalised, 512 = 16 x 2 x 16:
 //   pass 1   16-point DFTs over m of x[t + 32 m] in registers, twiddle W512^{t k1};
@@ -255,29 +318,32 @@ TFB_HD void wfft_forward(cd* x, int t, const Tw& tw, void* buf, W& w) {
   typename Tw::Chunk ch[2], chc;
   tw.issue4(0, ch[0]);  // lands while the first 16-point DFT runs
   if (FLIP) wflip_odd(x, (uint32_t)(t >> 4) << 31);
+  dft16_twisted(x);
+  // pass-1 twiddles folded into the cross-lane radix-2 stage: a lane multiplies only what it sends;
+  // what it keeps enters as  w x + got  (4 FMA),  w x - got = (w x + got) - 2 got  (2 FMA)
 #pragma unroll
-  for (int m = 1; m < WPTS; ++m) x[m] = cmul(x[m], twist16(m));
-  dft16<1>(x);
-#pragma unroll
-  for (int kb = 0; kb < WPTS; kb += 4) {
-    cd wk[4];
-    tw.settle4(ch[(kb >> 2) & 1], wk);
-    if (kb + 4 < WPTS)
-      tw.issue4(kb + 4, ch[((kb >> 2) + 1) & 1]);
+  for (int a = 0; a < 4; ++a) {
+    cd wk[4];  // twiddles of registers a, a+4, a+8, a+12
+    tw.settle4(ch[a & 1], wk);
+    if (a + 1 < 4)
+      tw.issue4(4 * (a + 1), ch[(a + 1) & 1]);
     else
       tw.issue_c(chc);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) x[kb + j] = cmul(x[kb + j], wk[j]);
+    for (int e = 0; e < 2; ++e) {
+      const int j = a + 4 * e;
+      const cd got = w.xchg16(cmul(x[8 + j], wk[2 + e]));
+      cd u0;
+      u0.re = fma(-wk[e].im, x[j].im, fma(wk[e].re, x[j].re, got.re));
+      u0.im = fma(wk[e].im, x[j].re, fma(wk[e].re, x[j].im, got.im));
+      x[j] = u0;
+      x[8 + j] = cd{fma(-2.0, got.re, u0.re), fma(-2.0, got.im, u0.im)};
+    }
   }
   {
     const cd c = tw.settle_c(chc);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const cd got = w.xchg16(x[8 + j]);
-      const cd u0 = cadd(x[j], got), u1 = csub(x[j], got);
-      x[j] = u0;
-      x[8 + j] = cmul(u1, c);
-    }
+    for (int j = 0; j < 8; ++j) x[8 + j] = cmul(x[8 + j], c);
   }
   wexchange<true>(x, t, buf, w);
   dft16<1>(x);
@@ -295,25 +361,30 @@ TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
   dft16<-1>(x);
   wexchange<false>(x, t, buf, w);
   {
-    const cd c = tw.settle_c(chc);
+    const cd c = tw.settle_c(chc), cc = cd{c.re, -c.im};
     tw.issue4(0, ch[0]);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const cd v = cmulc(x[8 + j], c);
-      const cd keep = cadd(x[j], v);
-      x[8 + j] = w.xchg16(csub(x[j], v));
+    for (int j = 0; j < 8; ++j) {  // keep x[j] + conj(c) x[8+j], send x[j] - conj(c) x[8+j]
+      cd keep, send;
+      bfly(x[j], x[8 + j], cc, keep, send);
+      x[8 + j] = w.xchg16(send);
       x[j] = keep;
     }
   }
+  // last 16-point DFT: the conjugate pass-1 twiddles ride in its first radix-4 layer (28 instead of
+  // 16 + 16 instructions per butterfly), the mid twiddles in the second; the register part of the twist
+  // multiplies the outputs (it depends on the output index, so it cannot be folded forward)
 #pragma unroll
-  for (int kb = 0; kb < WPTS; kb += 4) {
+  for (int a = 0; a < 4; ++a) {
     cd wk[4];
-    tw.settle4(ch[(kb >> 2) & 1], wk);
-    if (kb + 4 < WPTS) tw.issue4(kb + 4, ch[((kb >> 2) + 1) & 1]);
+    tw.settle4(ch[a & 1], wk);
+    if (a + 1 < 4) tw.issue4(4 * (a + 1), ch[(a + 1) & 1]);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) x[kb + j] = cmulc(x[kb + j], wk[j]);
+    for (int b = 0; b < 4; ++b) wk[b].im = -wk[b].im;
+    dft4_tw4<-1>(x[a], x[a + 4], x[a + 8], x[a + 12], wk[0], wk[1], wk[2], wk[3]);
   }
-  dft16<-1>(x);
+  dft16_layer_b<-1>(x);
+  transpose4x4(x);
 #pragma unroll
   for (int m = 1; m < WPTS; ++m) x[m] = cmulc(x[m], twist16(m));
   if (FLIP) wflip_odd(x, (uint32_t)(t >> 4) << 31);
@@ -462,7 +533,9 @@ TFB_HD void wcmux_stage(int s, const uint32_t* acc, int abar, int i, BkSource& b
   }
   wfft_forward<false>(x, t, tw, buf, w);
   const cd* chunk = bk.acquire_chunk(i, p, lvl);
+  w.turn_enter();
   wmac<FIRST>(park, x, bk, chunk, t);
+  w.turn_leave();
   bk.release();
 }
 
@@ -506,8 +579,15 @@ TFB_HD void gate_bootstrap_warp(const uint32_t* x_row, const uint32_t* y_row, in
 #pragma unroll 1
   for (int i = 0; i < n; ++i) {
     const int abar = sm_abar[i];
-    if (abar == 0) {  // uniform across the warp
-      bk.skip(i);
+    if (abar == 0) {  // uniform across the warp: X^0 - 1 = 0, the CMux is the identity
+      // keep the key ring and the turn protocol in step, in the order a real CMux takes them (a warp that
+      // held its turns back while it drained four chunks would stall the ring its partners wait on)
+#pragma unroll 1
+      for (int s = 0; s < 4; ++s) {
+        bk.acquire_chunk(i, s >> 1, s & 1);
+        w.turn_pass();
+        bk.release();
+      }
       continue;
     }
     wcmux_step(sm_acc, abar, i, bk, t, tw, buf, w, park);

@@ -175,6 +175,9 @@ struct EmuWarp {
   cd* scratch;  // 32 cd
   int lane;
   void operator()() const { pthread_barrier_wait(b); }
+  void turn_enter() const {}
+  void turn_leave() const {}
+  void turn_pass() const {}
   cd xchg16(cd v) const {
     scratch[lane] = v;
     pthread_barrier_wait(b);
