@@ -125,7 +125,8 @@ int tfb_debug_spectral_key(tfb_ctx *ctx, int32_t i, double *out_host);
 /* K1 dispatch, host logic only (no GPU needed): which fused-bootstrap variant a launch of k gates
  * takes on a device with `sms` multiprocessors.  Returns 1 = K1a (one gate per 64-thread CTA),
  * 2 = K1b (four gates per CTA, TMA key ring), 3 = K1c (one gate over four thread groups: latency),
- * 4 = K1d (one gate per warp, twelve per CTA: throughput).  When a large launch is split, *body_gates
+ * 4 = K1d (one gate per warp, twelve per CTA: throughput), 5 = K1e (one gate per two-CTA cluster: latency, launches of up
+ * to sms / 2 gates).  When a large launch is split, *body_gates
  * receives the number of leading gates that run as full K1d waves and the return value is the
  * variant of the remaining k - *body_gates gates; otherwise *body_gates = 0. */
 int tfb_debug_pick_kernel(int64_t k, int sms, int64_t *body_gates);

@@ -26,6 +26,7 @@
 #include "../../include/tfhe_b200.h"
 #include "tfhe_device.cuh"
 #include "tfhe_warp.cuh"
+#include "tfhe_cluster.cuh"
 
 using namespace tfb;
 
@@ -60,7 +61,7 @@ struct tfb_ctx {
   cudaEvent_t ev_in[HOST_EVENTS] = {}, ev_run[HOST_EVENTS] = {};
   int64_t launches = 0;
   int sm_count = 148;
-  int force_kernel = 0;        // 0 auto, 1 = K1a (one ciphertext per CTA), 2 = K1b (ring), 3 = K1c (wide), 4 = K1d (warp)
+  int force_kernel = 0;        // 0 auto, 1 = K1a (one ciphertext per CTA), 2 = K1b (ring), 3 = K1c (wide), 4 = K1d (warp), 5 = K1e (cluster pair)
   std::string err;
 };
 
@@ -1041,6 +1042,8 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gate_bootstrap_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, k1c_smem(p->n));
   if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k1e::k_gate_bootstrap_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, k1e::smem_bytes(p->n));
+  if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k2t::k_key_switch_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, k2t::SMEM_BYTES);
   if (e == cudaSuccess) {
     int sms = 0;
@@ -1118,19 +1121,21 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
   return TFB_OK;
 }
 
-// Cost model of the four K1 variants (ms per launch on a 148-SM B200 at n = 500, measured with
+// Cost model of the five K1 variants (ms per launch on a 148-SM B200 at n = 500, measured with
 // tools/k1_ab.py; only the ratios matter).  Every variant runs in waves of one CTA set per SM:
-//   K1c 1 gate / SM, 1.41 ms per wave        K1a up to 4 gates / SM, 2.49 .. 3.74 ms per wave
-//   K1b 4 gates / SM, 3.35 ms per wave       K1d 12 gates / SM, 8.6 ms per wave
-constexpr double K1D_WAVE_MS = 8.6;
+//   K1e 1 gate / 2 SMs (cluster), 1.05 ms per wave   K1c 1 gate / SM, 1.36 ms per wave
+//   K1a up to 4 gates / SM, 2.49 .. 3.74 ms per wave  K1b 4 gates / SM, 3.35 ms per wave
+//   K1d 12 gates / SM, 8.05 ms per wave
+constexpr double K1D_WAVE_MS = 8.05;
 static int pick_k1(int64_t k, int sms, double* cost) {
   const double S = (double)sms;
   const double waves_c = ceil(k / S), waves_b = ceil(k / (4 * S)), waves_d = ceil(k / (12 * S));
-  const double t[5] = {0.0,
+  const double waves_e = ceil(k / floor(S / 2));
+  const double t[6] = {0.0,
                        k <= S ? 2.49 : (k <= 2 * S ? 2.69 : (k <= 3 * S ? 3.53 : 3.74 * waves_b)),
-                       3.35 * waves_b, 1.41 * waves_c, K1D_WAVE_MS * waves_d};
+                       3.35 * waves_b, 1.36 * waves_c, K1D_WAVE_MS * waves_d, 1.05 * waves_e};
   int best = 3;
-  for (int w = 1; w <= 4; ++w)
+  for (int w = 1; w <= 5; ++w)
     if (t[w] < t[best]) best = w;
   if (cost) *cost = t[best];
   return best;
@@ -1139,7 +1144,10 @@ static int pick_k1(int64_t k, int sms, double* cost) {
 static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, int stride, const uint8_t* kinds,
                              const int32_t* xr, const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
   const int n = ctx->p.n;
-  if (which == 4) {
+  if (which == 5) {  // one gate per two-CTA cluster (the kernel carries __cluster_dims__(2, 1, 1))
+    k1e::k_gate_bootstrap_pair<<<(unsigned)(2 * k), k1e::THREADS, k1e::smem_bytes(n), st>>>(
+        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
+  } else if (which == 4) {
     const unsigned grid = (unsigned)((k + K1D_WARPS - 1) / K1D_WARPS);
     k_gate_bootstrap_warp<<<grid, K1D_THREADS, K1D_HEADER + K1D_WARPS * warp_smem(n), st>>>(
         (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ext, k);
@@ -1159,8 +1167,9 @@ static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, int stri
   return TFB_OK;
 }
 
-// K1 dispatch.  K1c (one gate over four thread groups) wins on latency, K1d (one gate per warp,
-// twelve per SM) on throughput, K1b / K1a in between.  A large launch runs its full K1d waves
+// K1 dispatch.  K1e (one gate per two-SM cluster) wins on latency while the launch fits half the chip, K1c
+// (one gate over four thread groups of one SM) up to one gate per SM, K1d (one gate per warp, twelve per SM) on
+// throughput, K1b / K1a in between.  A large launch runs its full K1d waves
 // first and hands the ragged rest to whichever variant finishes it soonest.
 // The split decision of launch_blind_rotate: variant of the tail (or of the whole launch when *body == 0).
 static int plan_k1(int64_t k, int sms, int64_t* body) {

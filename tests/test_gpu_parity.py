@@ -122,7 +122,8 @@ def test_edge_inputs_trivial_and_aliased(gpu, key, eval_keys):
 
 def test_every_kernel_variant_is_bit_exact(key, eval_keys, monkeypatch):
     """K1a (one gate per 64-thread CTA), K1b (four gates per CTA, TMA-staged key ring), K1c (one gate
-    over four thread groups), K1d (one gate per warp, twelve per CTA, tensor-memory parking) and the
+    over four thread groups), K1d (one gate per warp, twelve per CTA, tensor-memory parking), K1e (one gate per
+    two-CTA cluster, contributions exchanged through distributed shared memory) and the
     key-switch kernels (K2 direct / split with atomics on the IMAD pipe, K2t on the tensor cores) on the
     same jobs, with a gate count that leaves a ragged last CTA / a partial 128-gate tile."""
     import torch
@@ -131,7 +132,7 @@ def test_every_kernel_variant_is_bit_exact(key, eval_keys, monkeypatch):
 
     xs, ys, kinds, bits = make_inputs(key, 45, seed=36, kinds=(np.arange(45) % 9).astype(np.uint8))
     want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
-    for variant, ks in (("1", "1"), ("2", "2"), ("3", "1"), ("4", "2"), ("4", "1")):
+    for variant, ks in (("1", "1"), ("2", "2"), ("3", "1"), ("4", "2"), ("4", "1"), ("5", "1"), ("5", "2")):
         monkeypatch.setenv("TFB_FORCE_KERNEL", variant)
         monkeypatch.setenv("TFB_FORCE_KS", ks)  # 1 = K2 (IMAD pipe), 2 = K2t (tcgen05.mma kind::i8)
         ctx = _cabi.Context(0, key.params.m, key.params.mu.word, eval_keys.ring)
