@@ -465,6 +465,14 @@ struct WarpRing {
 #endif
 struct DevWarp {
   int turn_wait = 0, turn_next = 0;  // named-barrier ids (0: no protocol, e.g. the key-setup kernel)
+#ifdef TFB_K1D_PHASES
+  mutable long long T[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, last = 0;
+  __device__ __forceinline__ void tick(int k) const {
+    const long long now = clock64();
+    T[k] += now - last;
+    last = now;
+  }
+#endif
   __device__ __forceinline__ void turn_enter() const {
     if (TFB_K1D_TURNS && turn_wait) asm volatile("bar.sync %0, 64;" ::"r"(turn_wait) : "memory");
   }
@@ -688,7 +696,17 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
 #ifdef TFB_K1D_PROBE
   const long long probe_t0 = clock64();
 #endif
+#ifdef TFB_K1D_PHASES
+  w.last = clock64();
+#endif
   gate_bootstrap_warp(xr, yr, (int)kinds[g], n, mu, bk, ttw, acc, abar, buf, dst, t, w, park);
+#ifdef TFB_K1D_PHASES
+  if (t == 0 && blockIdx.x == 3 && (wid == 0 || wid == 5 || wid == 10))
+    printf("warp %2d per CMux: decomp/digits %lld | fwd burst1 %lld exch %lld burst2 %lld (x4) | key wait %lld turn wait %lld mac %lld (x4) | "
+           "inv: tmem %lld burst1 %lld exch %lld burst2 %lld update %lld (x2)\n",
+           wid, w.T[0] / n, w.T[1] / n, w.T[2] / n, w.T[3] / n, w.T[4] / n, w.T[5] / n, w.T[6] / n, w.T[7] / n, w.T[8] / n,
+           w.T[9] / n, w.T[10] / n, w.T[11] / n);
+#endif
 #ifdef TFB_K1D_PROBE
   if (t == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
     printf("cta %d warp %2d: %lld cycles, %lld waiting for the key (%.1f%%), %lld polls\n", (int)blockIdx.x, wid,

@@ -30,6 +30,12 @@
 #define TFB_K1D_LOOP _Pragma("unroll")
 #endif
 
+#ifdef TFB_K1D_PHASES  // per-phase clock probe (a profiling build): W::tick(k) accumulates cycles since the last tick
+#define TFB_TICK(w, k) (w).tick(k)
+#else
+#define TFB_TICK(w, k)
+#endif
+
 namespace tfb {
 
 constexpr int WARP_T = 32;  // lanes per ciphertext
@@ -318,6 +324,7 @@ TFB_HD void wfft_forward(cd* x, int t, const Tw& tw, void* buf, W& w) {
   typename Tw::Chunk ch[2], chc;
   tw.issue4(0, ch[0]);  // lands while the first 16-point DFT runs
   if (FLIP) wflip_odd(x, (uint32_t)(t >> 4) << 31);
+  TFB_TICK(w, 0);
   dft16_twisted(x);
   // pass-1 twiddles folded into the cross-lane radix-2 stage: a lane multiplies only what it sends;
   // what it keeps enters as  w x + got  (4 FMA),  w x - got = (w x + got) - 2 got  (2 FMA)
@@ -345,8 +352,11 @@ TFB_HD void wfft_forward(cd* x, int t, const Tw& tw, void* buf, W& w) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) x[8 + j] = cmul(x[8 + j], c);
   }
+  TFB_TICK(w, 1);
   wexchange<true>(x, t, buf, w);
+  TFB_TICK(w, 2);
   dft16<1>(x);
+  TFB_TICK(w, 3);
 }
 
 // Inverse of wfft_forward up to the factor 512 (folded into the key): the conjugate transpose,
@@ -358,8 +368,11 @@ template <bool FLIP = true, class W, class Tw>
 TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
   typename Tw::Chunk ch[2], chc;
   tw.issue_c(chc);
+  TFB_TICK(w, 7);
   dft16<-1>(x);
+  TFB_TICK(w, 8);
   wexchange<false>(x, t, buf, w);
+  TFB_TICK(w, 9);
   {
     const cd c = tw.settle_c(chc), cc = cd{c.re, -c.im};
     tw.issue4(0, ch[0]);
@@ -387,6 +400,7 @@ TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
   transpose4x4(x);
 #pragma unroll
   for (int m = 1; m < WPTS; ++m) x[m] = cmulc(x[m], twist16(m));
+  TFB_TICK(w, 10);
   if (FLIP) wflip_odd(x, (uint32_t)(t >> 4) << 31);
 }
 
@@ -533,10 +547,13 @@ TFB_HD void wcmux_stage(int s, const uint32_t* acc, int abar, int i, BkSource& b
   }
   wfft_forward<false>(x, t, tw, buf, w);
   const cd* chunk = bk.acquire_chunk(i, p, lvl);
+  TFB_TICK(w, 4);
   w.turn_enter();
+  TFB_TICK(w, 5);
   wmac<FIRST>(park, x, bk, chunk, t);
   w.turn_leave();
   bk.release();
+  TFB_TICK(w, 6);
 }
 
 // One CMux step by one warp.  acc: 2 polynomials of N words in shared memory.
@@ -565,6 +582,7 @@ TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, cons
       acc[c * RING_N + t + 32 * m] += (m & 1) ? round_to_word_signed(x[m].re, sg) : round_to_word(x[m].re);
       acc[c * RING_N + t + 32 * m + HALF_N] += (m & 1) ? round_to_word_signed(x[m].im, sg) : round_to_word(x[m].im);
     }
+    TFB_TICK(w, 11);
   }
   w();
 }
