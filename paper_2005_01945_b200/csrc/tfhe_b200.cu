@@ -115,7 +115,6 @@ struct LdgBk {
     return cd{v.x, v.y};
   }
   __device__ __forceinline__ void release() {}
-  __device__ __forceinline__ void skip(int) {}
 };
 
 // ---- mbarrier / bulk-copy (TMA) primitives --------------------------------------------
@@ -243,6 +242,22 @@ constexpr int K1B_SLOTS = TFB_K1B_SLOTS;
 // dynamic smem: twiddles | ring[K1B_SLOTS][STAGE_CD] | mbarriers (64 B) | groups
 constexpr int K1B_HEADER = (int)sizeof(Twiddles) + K1B_SLOTS * STAGE_BYTES + 64;
 
+#ifndef TFB_K1B_TURNS
+#define TFB_K1B_TURNS 1
+#endif
+struct TurnPark {  // no parking; a two-party turn rotation on named barriers (64 threads arrive, 64 wait)
+  static constexpr bool parks = false;
+  int wait_id, next_id;
+  __device__ __forceinline__ void store(const cd*, const cd*) {}
+  __device__ __forceinline__ void load(int, cd&, cd&) {}
+  __device__ __forceinline__ void turn_enter() const { asm volatile("bar.sync %0, 128;" ::"r"(wait_id) : "memory"); }
+  __device__ __forceinline__ void turn_leave() const { asm volatile("bar.arrive %0, 128;" ::"r"(next_id) : "memory"); }
+  __device__ __forceinline__ void turn_pass() const {
+    turn_enter();
+    turn_leave();
+  }
+};
+
 struct RingBk {
   const cd* bkf;       // full spectral key in global memory
   cd* ring;            // K1B_SLOTS stages in shared memory
@@ -279,12 +294,6 @@ struct RingBk {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot(stage)]);
     ++stage;
-  }
-  __device__ __forceinline__ void skip(int) {
-    acquire(0, 0);
-    release();
-    acquire(0, 1);
-    release();
   }
 };
 
@@ -327,7 +336,15 @@ __global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
   const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
   uint32_t* dst = want < k ? ext + g * EXT_STRIDE : reinterpret_cast<uint32_t*>(s0);  // scratch sink
   GroupSync sync{grp + 1};
+#if TFB_K1B_TURNS
+  // groups g and g + 2 put one warp each on the same two schedulers (warp w runs on scheduler w % 4): they take the
+  // MAC of a CMux half in turns (the K1d rotation, DevWarp below, with two parties)
+  static_assert(K1B_GROUPS == 4, "the turn pairs are laid out for four groups");
+  TurnPark park{8 + 2 * (grp & 1) + ((grp >> 1) ^ 1), 8 + 2 * (grp & 1) + (grp >> 1)};
+  if (grp >> 1) park.turn_leave();
+#else
   NoPark park;
+#endif
   gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, dst, t, sync, park);
 }
 

@@ -390,15 +390,14 @@ TFB_HD int stage_index(int k2, int lvl, int c, int t) { return ((k2 * BK_L + lvl
 //   const cd* acquire(i, p)   pointer to the stage (blocks until it is resident)
 //   cd load(q)                one value of it
 //   void release()            this thread is done with the stage
-//   void skip(i)              the CMux of index i is skipped (abar == 0); keeps a
-//                             staged pipeline's bookkeeping in step
+// (a skipped CMux -- abar == 0 -- still acquires and releases its stages, so that a staged pipeline's
+// bookkeeping stays in step)
 struct GlobalBk {  // plain pointer into the full key (host emulation, key setup checks)
   const cd* base;
   TFB_HD const cd* acquire(int i, int p) { return base + stage_offset(i, p); }
   TFB_HD const cd* acquire_chunk(int i, int p, int lvl) { return base + stage_offset(i, p) + (size_t)lvl * (STAGE_CD / 2); }
   TFB_HD cd load(const cd* q) const { return *q; }
   TFB_HD void release() {}
-  TFB_HD void skip(int) {}
 };
 
 // acc: 2 polynomials of N words in shared memory ([0..N) = a, [N..2N) = b).
@@ -412,10 +411,15 @@ struct GlobalBk {  // plain pointer into the full key (host emulation, key setup
 // A Park policy may hold the 16 accumulator values of a thread outside the register file
 // between the two halves of a CMux (the B200 kernel parks them in tensor memory):
 //   store(out0, out1) after the first half, load(k2, o0, o1) inside the second half's MAC.
+// A policy may also order the MAC stages of the groups that share schedulers (turn_enter / turn_leave /
+// turn_pass; see TurnPark in tfhe_b200.cu).
 struct NoPark {
   static constexpr bool parks = false;
   TFB_HD void store(const cd*, const cd*) {}
   TFB_HD void load(int, cd&, cd&) {}
+  TFB_HD void turn_enter() const {}
+  TFB_HD void turn_leave() const {}
+  TFB_HD void turn_pass() const {}
 };
 
 template <int P, class Sync, class BkSource, class Park>
@@ -431,6 +435,7 @@ TFB_HD void cmux_half(cd* out0, cd* out1, const uint32_t* acc, int abar, int i, 
   }
   fft_forward2<P>(x0, x1, t, tw, s0, s1, sync);
   const cd* stage = bk.acquire(i, P);
+  park.turn_enter();
 #pragma unroll
   for (int k2 = 0; k2 < 8; ++k2) {
     if (P == 0) {
@@ -444,6 +449,7 @@ TFB_HD void cmux_half(cd* out0, cd* out1, const uint32_t* acc, int abar, int i, 
     cmac(out0[k2], x1[k2], bk.load(stage + stage_index(k2, 1, 0, t)));
     cmac(out1[k2], x1[k2], bk.load(stage + stage_index(k2, 1, 1, t)));
   }
+  park.turn_leave();
   bk.release();
 }
 
@@ -527,8 +533,12 @@ TFB_HD void gate_bootstrap(const uint32_t* x_row, const uint32_t* y_row, int kin
 #pragma unroll 1
   for (int i = 0; i < n; ++i) {
     const int abar = sm_abar[i];
-    if (abar == 0) {  // uniform across the group
-      bk.skip(i);
+    if (abar == 0) {  // uniform across the group: keep the key pipeline and the turn order in step
+      for (int p = 0; p < 2; ++p) {
+        bk.acquire(i, p);
+        park.turn_pass();
+        bk.release();
+      }
       continue;
     }
     cmux_step(sm_acc, abar, i, bk, t, tw, s0, s1, sync, park);

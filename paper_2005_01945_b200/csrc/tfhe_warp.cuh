@@ -407,7 +407,7 @@ TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
 // Spectral key stage (i, p) in this kernel's order: [lvl][q][c][lane], prescaled by 1/512
 // (same 32 KB per stage and the same stage_offset as the 64-thread layout).  The unit the
 // key ring moves is a CHUNK = one (i, p, lvl) = 16 KB: what one MAC consumes.  A key source
-// offers acquire_chunk(i, p, lvl) / load(ptr) / release() / skip(i).
+// offers acquire_chunk(i, p, lvl) / load(ptr) / release().
 constexpr int WCHUNK_CD = WPTS * 2 * WARP_T;  // 1024 cd
 TFB_HD int wstage_index(int lvl, int q, int c, int t) { return ((lvl * WPTS + q) * 2 + c) * WARP_T + t; }
 
