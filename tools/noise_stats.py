@@ -52,6 +52,9 @@ for kind in (GateKind.NAND, GateKind.XOR):
             "std": float(e.std()), "max_abs": float(np.abs(e).max()), "mean": float(e.mean()),
             "exceed_fresh_bound": int((np.abs(e) >= eng.fresh_bound).sum()),
             "sigmas_to_bound": float(eng.fresh_bound / e.std()),
+            "count": int(e.size),
+            # tail counts against the Gaussian prediction 2 Q(z) * count (the bound sits at ~6.4 sigma)
+            "tail_counts": {f"{z}": int((np.abs(e - e.mean()) > z * e.std()).sum()) for z in (4.0, 4.5, 5.0, 5.5, 6.0)},
         }
         print(kind.value, level, report[f"{kind.value}_level{level}"], flush=True)
 os.makedirs(os.path.dirname(args.out), exist_ok=True)
