@@ -133,6 +133,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) k_gate_b
   const uint32_t recv_peer = peer_address((uint32_t)__cvta_generic_to_shared(recv), peer);
   const uint32_t bars_peer = peer_address(bars_local, peer);
   uint32_t done = 0;  // CMux steps executed so far: buffer = done & 1, phase parity = (done >> 1) & 1
+  cd b_keep[8], b_give[8];
+  int loaded_for = -1;
+  auto load_key = [&](int i) {
+    const cd* stage = bkf + stage_offset(i, (int)p);
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) {
+      const double2 u = __ldg(reinterpret_cast<const double2*>(stage + stage_index(k2, grp, c_keep, t)));
+      const double2 v = __ldg(reinterpret_cast<const double2*>(stage + stage_index(k2, grp, c_keep ^ 1, t)));
+      b_keep[k2] = cd{u.x, u.y};
+      b_give[k2] = cd{v.x, v.y};
+    }
+    loaded_for = i;
+  };
 #ifdef TFB_K1E_PROBE
   long long T[8] = {0, 0, 0, 0, 0, 0, 0, 0}, c0 = clock64(), c1;
 #define K1E_TICK(k) c1 = clock64(); T[k] += c1 - c0; c0 = c1;
@@ -148,16 +161,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) k_gate_b
     if (tid == 0)  // arm this step's receive: 4 KB from the peer's group 1
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bars_local + 8u * buf), "r"(RECV_WORDS * 4)
                    : "memory");
-    // key stage (i, p), level grp, both output components: in flight while the transform runs
-    const cd* stage = bkf + stage_offset(i, (int)p);
-    cd b_keep[8], b_give[8];
-#pragma unroll
-    for (int k2 = 0; k2 < 8; ++k2) {
-      const double2 u = __ldg(reinterpret_cast<const double2*>(stage + stage_index(k2, grp, c_keep, t)));
-      const double2 v = __ldg(reinterpret_cast<const double2*>(stage + stage_index(k2, grp, c_keep ^ 1, t)));
-      b_keep[k2] = cd{u.x, u.y};
-      b_give[k2] = cd{v.x, v.y};
-    }
+    // key stage (i, p), level grp, both output components: normally already in flight (requested right after the
+    // previous step's products); loaded here for the first step and after a skipped one
+    if (loaded_for != i) load_key(i);
     K1E_TICK(0)
     cd x[8];
 #pragma unroll
@@ -174,6 +180,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1) k_gate_b
       swap[(grp * 8 + k2) * FFT_THREADS + t] = cmul(x[k2], b_give[k2]);
       x[k2] = cmul(x[k2], b_keep[k2]);
     }
+    if (i + 1 < n) load_key(i + 1);  // the next step's key travels during the inverse transform and the exchange
     K1E_TICK(3)
     __syncthreads();
     K1E_TICK(4)

@@ -656,6 +656,7 @@ class B200Engine(GateEngine):
         self.device = torch.device("cuda", self.device_index)
         self._pool_t = torch.zeros((initial_rows, _cabi.ROW_STRIDE), dtype=torch.int32, device=self.device)
         self._pending: list = []  # (first row, packed host words) awaiting upload
+        self._stage = None
         super().__init__(key.params, pool)
         self._enc_rng = np.random.default_rng((self.seed, self._ENC_STREAM))
         # device_encrypt: fresh encryptions drawn on the GPU by a counter-based generator (throughput inputs:
@@ -709,9 +710,37 @@ class B200Engine(GateEngine):
     # -- evaluation -------------------------------------------------------------------------
     EVAL_CHUNK = 1 << 18  # gates per tfb_gate_launch: bounds the library's extracted-sample scratch at 1.1 GB
 
+    STAGE_GATES = 4096  # launches up to this size send their index arrays through one pinned staging copy
+
+    def _stage_small(self, kind_ids, x_rows, y_rows, out_rows):
+        """Index arrays + kinds of a narrow launch in ONE host->device copy from pinned memory (the latency path issues
+        a launch per gate level: two pageable copies per level were ~5 % of a level).  Staging slots rotate, so a slot
+        is rewritten long after the copy that read it was ordered before later work on the stream."""
+        torch, k = self._torch, len(kind_ids)
+        if self._stage is None:
+            words = 4 * self.STAGE_GATES  # x, y, out (int32 each) + kinds (uint8, padded to a word each 4)
+            self._stage = [(torch.empty(words, dtype=torch.int32).pin_memory(),
+                            torch.empty(words, dtype=torch.int32, device=self.device)) for _ in range(8)]
+            self._stage_at = 0
+        host, dev = self._stage[self._stage_at]
+        self._stage_at = (self._stage_at + 1) % len(self._stage)
+        if self._stage_at == 0:
+            torch.cuda.current_stream(self.device).synchronize()  # every slot's last copy has completed before reuse
+        h = host.numpy()
+        h[:k], h[k : 2 * k], h[2 * k : 3 * k] = x_rows, y_rows, out_rows
+        h[3 * k : 3 * k + (k + 3) // 4].view(np.uint8)[:k] = kind_ids
+        n = 3 * k + (k + 3) // 4
+        dev[:n].copy_(host[:n], non_blocking=True)
+        return dev.data_ptr(), dev.data_ptr() + 12 * k
+
     def _evaluate(self, kind_ids, x_rows, y_rows, out_rows) -> None:
         self._flush()
         k = len(kind_ids)
+        if k <= self.STAGE_GATES:
+            base, kinds_ptr = self._stage_small(kind_ids, x_rows, y_rows, out_rows)
+            self._ctx.call("tfb_gate_launch", self._pool_t.data_ptr(), kinds_ptr, base, base + 4 * k, base + 8 * k, k,
+                           self._stream())
+            return
         idx = self._dev(np.concatenate([x_rows, y_rows, out_rows]), np.int32)
         kinds = self._dev(kind_ids, np.uint8)
         base, step = idx.data_ptr(), 4 * k
