@@ -46,8 +46,14 @@ METRIC = "bootstrapped_gates_per_sec"
 UNIT = "gates/s"
 KEY_SEED, ENGINE_SEED = 2024, 42
 NAND = 2
-# 500 iterations x (6 negacyclic transforms of 26,112 FLOP + 8 x 512 complex MACs) per gate
-FLOP_PER_GATE = 500 * (6 * 26112 + 32768)
+# Algorithmic FP64 work of one gate with the bootstrapping key unrolled over pairs of mask elements (SURVEY 8(d)'s count
+# restated for 250 pair steps instead of 500 CMux steps): per step 6 negacyclic transforms of 26,112 FLOP (radix-2 count
+# incl. the twist) and, per spectral point (512) and digit polynomial (4), the key combination K = u1 B1 + u2 B2 + u1 u2 B12
+# for both output components (2 x 3 complex multiply-adds = 48 FLOP) and the two MACs (16 FLOP), plus the two rotation
+# factors once per point (14 FLOP): 156,672 + 512 x (4 x 64 + 14) = 294,912 FLOP per step, 73.73 MFLOP per gate.
+# (The plain CMux loop of round 1 was 500 x (6 x 26,112 + 32,768) = 94.72 MFLOP per gate.)
+FLOP_PER_GATE = 250 * (6 * 26112 + 512 * (4 * 64 + 14))
+FLOP_PER_GATE_PLAIN_CMUX = 500 * (6 * 26112 + 32768)
 SHARDED = {"vec_add": (4096, 32), "vec_mul": (4096, 32), "matmul16": (16, 16)}  # (lanes | rank, bit width)
 
 
@@ -68,7 +74,7 @@ def parse_args():
 
 def config(args, n_gpus):
     cfg = {
-        "params": "m=500 alpha=2^-15 w=32 mu=1/8; ring N=1024 k=1 l=2 Bg=2^10 ks t=8 base=4",
+        "params": "m=500 alpha=2^-15 w=32 mu=1/8; ring N=1024 k=1 l=2 Bg=2^9 ks t=8 base=4; bootstrapping key unrolled over pairs of mask elements (250 blind-rotation steps)",
     }
     if args.workload == "gates":
         cfg.update({
@@ -757,6 +763,9 @@ def run_b200(args) -> None:
             "bound": "fp64", "achieved": k1_tflops, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
             "frac": k1_tflops / peaks["fp64_tflops"], "traffic": traffic, "traffic_source": traffic_src,
             "flop_per_gate": FLOP_PER_GATE, "ms_per_launch": k1_ms, "gates_per_launch": k1_gates,
+            # the same launch rated by the work a plain (not unrolled) CMux loop would need: what rounds 1-2a reported
+            "flop_per_gate_plain_cmux": FLOP_PER_GATE_PLAIN_CMUX,
+            "frac_at_plain_cmux_count": k1_gates * FLOP_PER_GATE_PLAIN_CMUX / (k1_ms * 1e-3) / 1e12 / peaks["fp64_tflops"],
             "share_of_step": (k1_ms / head["ms_per_step"]) if args.workload == "gates" else None,
             "peak_source": "measured in this run: dependent-free DFMA loop on all SMs (tfb_measure_peaks); "
                            "MEASURED_PEAKS.json has no FP64 figure",

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TFB_ABI_VERSION 1
+#define TFB_ABI_VERSION 2
 #define TFB_ROW_STRIDE 512  /* uint32 words per pool row */
 #define TFB_EXT_STRIDE 1032 /* uint32 words per extracted (N+1)-word sample */
 
@@ -49,9 +49,10 @@ enum {
 
 /* Parameter set.  LWE side from encirc/torus.py:25-27,118-134; ring side is the
  * builder's choice (the reference has none) and only this set is compiled:
- * ring_n 1024, bk_l 2, bk_bgbit 10, ks_t 8, ks_basebit 2. */
+ * ring_n 1024, bk_l 2, bk_bgbit 9, ks_t 8, ks_basebit 2, bootstrapping key unrolled
+ * over pairs of mask elements (three TRGSW samples per pair). */
 typedef struct tfb_params {
-  int32_t n;          /* LWE dimension m (<= 511) */
+  int32_t n;          /* LWE dimension m (<= 510) */
   int32_t ring_n;     /* TRLWE degree N */
   int32_t bk_l;       /* gadget length */
   int32_t bk_bgbit;   /* log2 gadget base */
@@ -71,8 +72,9 @@ const char *tfb_last_error(const tfb_ctx *ctx); /* ctx may be NULL: last creatio
 int tfb_ctx_create(int device, const tfb_params *params, tfb_ctx **out);
 void tfb_ctx_destroy(tfb_ctx *ctx);
 
-/* Key setup (kernel K3).  bk: int32[n][4][2][N] raw TRGSW rows, ksk:
- * int32[N][8][n+1] raw LWE rows (layouts in paper_2005_01945_b200/keys.py).
+/* Key setup (kernel K3).  bk: int32[ceil(n/2)][3][4][2][N] raw TRGSW rows (pair of mask
+ * elements, key s1 / s2 / s1*s2, row, component), ksk: int32[N][8][n+1] raw LWE rows
+ * (layouts in paper_2005_01945_b200/keys.py).
  * on_device != 0 means both pointers are device pointers (e.g. the receive
  * buffers of an NCCL broadcast).  Transforms bk to the FFT domain in the
  * kernel's register order and lays ksk out row-padded for coalesced loads. */
@@ -118,15 +120,13 @@ int tfb_debug_blind_rotate(tfb_ctx *ctx, const void *pool_dev, const uint8_t *ki
                            int64_t k, void *stream);
 int tfb_debug_key_switch(tfb_ctx *ctx, const uint32_t *ext_dev, void *pool_dev, const int32_t *out_rows_dev,
                          int64_t k, void *stream);
-/* Spectral key of LWE index i, de-permuted to natural frequency order and
- * un-scaled: double[4][2][512][2] (row, component, frequency, re/im). */
-int tfb_debug_spectral_key(tfb_ctx *ctx, int32_t i, double *out_host);
+/* Spectral key `key` (0: s1, 1: s2, 2: s1*s2) of mask-element pair `pair`, de-permuted to
+ * natural frequency order and un-scaled: double[4][2][512][2] (row, component, frequency, re/im). */
+int tfb_debug_spectral_key(tfb_ctx *ctx, int32_t pair, int32_t key, double *out_host);
 
 /* K1 dispatch, host logic only (no GPU needed): which fused-bootstrap variant a launch of k gates
- * takes on a device with `sms` multiprocessors.  Returns 1 = K1a (one gate per 64-thread CTA),
- * 2 = K1b (four gates per CTA, TMA key ring), 3 = K1c (one gate over four thread groups: latency),
- * 4 = K1d (one gate per warp, twelve per CTA: throughput), 5 = K1e (one gate per two-CTA cluster: latency, launches of up
- * to sms / 2 gates).  When a large launch is split, *body_gates
+ * takes on a device with `sms` multiprocessors.  Returns 4 = K1d (one gate per warp, twelve per CTA:
+ * throughput) or 5 = K1e (one gate per two-CTA cluster: latency).  When a large launch is split, *body_gates
  * receives the number of leading gates that run as full K1d waves and the return value is the
  * variant of the remaining k - *body_gates gates; otherwise *body_gates = 0. */
 int tfb_debug_pick_kernel(int64_t k, int sms, int64_t *body_gates);

@@ -20,7 +20,16 @@
  * (encirc/torus.py:177-184).
  *
  * Parameter set (ring side chosen by the builder): N = 1024,
- * k = 1, l = 2, Bg = 2^10, key switch t = 8, base 4, signed digits.
+ * k = 1, l = 2, Bg = 2^9 (rounded to 18 bits), key switch t = 8, base 4, signed digits.
+ *
+ * Blind rotation with an UNROLLED bootstrapping key (Zhou, Yang, Zhang, Yang, Wang:
+ * "Faster bootstrapping with multiple addends", IEEE Access 2018; Bourse, Minelli, Minihold,
+ * Paillier, CRYPTO 2018 section 5): two LWE mask elements per CMux.  With key bits s1, s2 and
+ * rotations a1, a2,  X^(a1 s1 + a2 s2) - 1 = s1 u1 + s2 u2 + s1 s2 u1 u2,  u_i = X^(a_i) - 1,
+ * so one step is
+ *   ACC <- ACC + u1 (BK[s1] [.] ACC) + u2 (BK[s2] [.] ACC) + u1 u2 (BK[s1 s2] [.] ACC)
+ * with ONE gadget decomposition of ACC shared by the three external products: n/2 steps of
+ * four forward and two inverse transforms instead of n.  An odd n pads s2 = 0, a2 = 0.
  *
  * A second blind-rotation path (`fft` = 1) evaluates the external product
  * with a textbook radix-2 double-precision FFT, as CPU TFHE libraries do.  It
@@ -37,7 +46,8 @@
 #define RN 1024
 #define HN 512
 #define BK_L 2
-#define BGBIT 10
+#define BGBIT 9
+#define BK_KEYS 3 /* TRGSW samples per pair of mask elements: s1, s2, s1*s2 */
 #define ROWS 4
 #define KS_T 8
 #define KS_BB 2
@@ -84,6 +94,7 @@ static void negacyclic_mac(uint32_t *res, const int32_t *d, const uint32_t *b) {
 static void decompose(const uint32_t *p, int32_t dec[BK_L][RN]) {
   uint32_t offset = 0;
   for (int l = 0; l < BK_L; ++l) offset += (uint32_t)(1u << (BGBIT - 1)) << (32 - (l + 1) * BGBIT);
+  offset += 1u << (32 - BK_L * BGBIT - 1); /* round to the nearest multiple of Bg^-l instead of truncating */
   for (int j = 0; j < RN; ++j) {
     const uint32_t v = p[j] + offset;
     for (int l = 0; l < BK_L; ++l)
@@ -95,6 +106,7 @@ static void decompose(const uint32_t *p, int32_t dec[BK_L][RN]) {
 typedef struct { double re, im; } cplx;
 static cplx g_tw[HN];     /* exp(2 pi i k / 512) */
 static cplx g_twist[HN];  /* exp(i pi j / N) */
+static cplx g_root[2 * RN]; /* exp(i pi m / N): X^e at spectral point f is g_root[e (1 + 4 f) mod 2N] */
 static int g_fft_ready = 0;
 
 static void fft_setup(void) {
@@ -105,6 +117,10 @@ static void fft_setup(void) {
     g_tw[k].im = (double)sinl(2 * pi * k / HN);
     g_twist[k].re = (double)cosl(pi * k / RN);
     g_twist[k].im = (double)sinl(pi * k / RN);
+  }
+  for (int m = 0; m < 2 * RN; ++m) {
+    g_root[m].re = (double)cosl(pi * m / RN);
+    g_root[m].im = (double)sinl(pi * m / RN);
   }
   g_fft_ready = 1;
 }
@@ -150,47 +166,79 @@ static void spec_add_to_poly(cplx *z, uint32_t *p) {
   }
 }
 
-/* spectral copy of the bootstrapping key for the fft path: [n][ROWS][2][HN] */
+/* spectral copy of the bootstrapping key for the fft path: [pairs][BK_KEYS][ROWS][2][HN] */
 cplx *oracle_bk_to_spectral(const int32_t *bk, int n) {
   fft_setup();
-  cplx *out = (cplx *)malloc((size_t)n * ROWS * 2 * HN * sizeof(cplx));
-  for (int64_t q = 0; q < (int64_t)n * ROWS * 2; ++q) poly_to_spec(bk + q * RN, out + q * HN);
+  const int64_t polys = (int64_t)((n + 1) / 2) * BK_KEYS * ROWS * 2;
+  cplx *out = (cplx *)malloc((size_t)polys * HN * sizeof(cplx));
+  for (int64_t q = 0; q < polys; ++q) poly_to_spec(bk + q * RN, out + q * HN);
   return out;
 }
 void oracle_free(void *p) { free(p); }
 
+/* acc += (X^e - 1) * p, all mod 2^32 */
+static void add_rotated_diff(uint32_t *acc, const uint32_t *p, int e) {
+  uint32_t rot[RN];
+  mul_by_xe(rot, p, e);
+  for (int j = 0; j < RN; ++j) acc[j] += rot[j] - p[j];
+}
+
 /* Blind rotation + sample extract.  bar: n+1 mod-switched words (last = body).
- * bk: int32[n][ROWS][2][N].  bk_spec: NULL for the exact path.  ext: N+1 words. */
+ * bk: int32[(n+1)/2][BK_KEYS][ROWS][2][N], key 0 = TRGSW(s_{2m}), 1 = TRGSW(s_{2m+1}), 2 = TRGSW(s_{2m} s_{2m+1}).
+ * bk_spec: NULL for the exact path.  ext: N+1 words. */
 void oracle_blind_rotate(const int32_t *bar, int n, uint32_t mu, const int32_t *bk, const cplx *bk_spec,
                          uint32_t *ext) {
-  uint32_t acc[2][RN], rot[RN], diff[RN], tv[RN];
+  uint32_t acc[2][RN], tv[RN];
   int32_t dec[ROWS][RN];
   for (int j = 0; j < RN; ++j) { acc[0][j] = 0; tv[j] = mu; }
   mul_by_xe(acc[1], tv, (2 * RN - bar[n]) % (2 * RN));
-  for (int i = 0; i < n; ++i) {
-    const int e = bar[i];
-    if (e == 0) continue;
-    for (int p = 0; p < 2; ++p) {
-      mul_by_xe(rot, acc[p], e);
-      for (int j = 0; j < RN; ++j) diff[j] = rot[j] - acc[p][j];
-      decompose(diff, &dec[p * BK_L]);
-    }
+  for (int m = 0; 2 * m < n; ++m) {
+    const int a1 = bar[2 * m], a2 = (2 * m + 1 < n) ? bar[2 * m + 1] : 0;
+    if (a1 == 0 && a2 == 0) continue;
+    for (int p = 0; p < 2; ++p) decompose(acc[p], &dec[p * BK_L]);
     if (!bk_spec) {
-      for (int r = 0; r < ROWS; ++r)
-        for (int c = 0; c < 2; ++c)
-          negacyclic_mac(acc[c], dec[r], (const uint32_t *)bk + (((size_t)i * ROWS + r) * 2 + c) * RN);
-    } else {
-      cplx d[ROWS][HN], o[2][HN];
-      for (int r = 0; r < ROWS; ++r) poly_to_spec(dec[r], d[r]);
-      memset(o, 0, sizeof o);
-      for (int r = 0; r < ROWS; ++r)
+      for (int j = 0; j < BK_KEYS; ++j) {
+        if ((j == 0 && a1 == 0) || (j == 1 && a2 == 0) || (j == 2 && (a1 == 0 || a2 == 0))) continue; /* factor is 0 */
+        uint32_t prod[2][RN];
+        memset(prod, 0, sizeof prod);
+        for (int r = 0; r < ROWS; ++r)
+          for (int c = 0; c < 2; ++c)
+            negacyclic_mac(prod[c], dec[r], (const uint32_t *)bk + ((((size_t)m * BK_KEYS + j) * ROWS + r) * 2 + c) * RN);
         for (int c = 0; c < 2; ++c) {
-          const cplx *b = bk_spec + (((size_t)i * ROWS + r) * 2 + c) * HN;
-          for (int f = 0; f < HN; ++f) {
-            o[c][f].re += d[r][f].re * b[f].re - d[r][f].im * b[f].im;
-            o[c][f].im += d[r][f].re * b[f].im + d[r][f].im * b[f].re;
+          if (j < 2) {
+            add_rotated_diff(acc[c], prod[c], j == 0 ? a1 : a2);
+          } else { /* (X^a1 - 1)(X^a2 - 1) */
+            uint32_t q[RN];
+            memset(q, 0, sizeof q);
+            add_rotated_diff(q, prod[c], a1);
+            add_rotated_diff(acc[c], q, a2);
           }
         }
+      }
+    } else {
+      static __thread cplx d[ROWS][HN], o[2][HN];
+      for (int r = 0; r < ROWS; ++r) poly_to_spec(dec[r], d[r]);
+      for (int f = 0; f < HN; ++f) {
+        const cplx w1 = g_root[(a1 * (1 + 4 * f)) & (2 * RN - 1)], w2 = g_root[(a2 * (1 + 4 * f)) & (2 * RN - 1)];
+        const cplx u1 = {w1.re - 1.0, w1.im}, u2 = {w2.re - 1.0, w2.im};
+        const cplx u12 = {u1.re * u2.re - u1.im * u2.im, u1.re * u2.im + u1.im * u2.re};
+        const cplx fac[BK_KEYS] = {u1, u2, u12};
+        for (int c = 0; c < 2; ++c) {
+          double sre = 0, sim = 0;
+          for (int j = 0; j < BK_KEYS; ++j) {
+            double pre = 0, pim = 0;
+            for (int r = 0; r < ROWS; ++r) {
+              const cplx *b = bk_spec + ((((size_t)m * BK_KEYS + j) * ROWS + r) * 2 + c) * HN;
+              pre += d[r][f].re * b[f].re - d[r][f].im * b[f].im;
+              pim += d[r][f].re * b[f].im + d[r][f].im * b[f].re;
+            }
+            sre += fac[j].re * pre - fac[j].im * pim;
+            sim += fac[j].re * pim + fac[j].im * pre;
+          }
+          o[c][f].re = sre;
+          o[c][f].im = sim;
+        }
+      }
       for (int c = 0; c < 2; ++c) spec_add_to_poly(o[c], acc[c]);
     }
   }

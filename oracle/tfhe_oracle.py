@@ -83,7 +83,7 @@ def gate_bootstrap_batch(x, y, kinds, mu: int, bk: np.ndarray, ksk: np.ndarray, 
     n = n1 - 1
     bk = np.ascontiguousarray(bk, dtype=np.int32)
     ksk = np.ascontiguousarray(ksk, dtype=np.int32)
-    assert bk.shape == (n, 4, 2, RING_N) and ksk.shape == (RING_N, 8, n + 1)
+    assert bk.shape == ((n + 1) // 2, 3, 4, 2, RING_N) and ksk.shape == (RING_N, 8, n + 1)
     out = np.empty((k, n + 1), dtype=np.uint32)
     ext = np.empty((k, RING_N + 1), dtype=np.uint32) if want_ext else None
     bar = np.empty((k, n + 1), dtype=np.int32) if want_bar else None

@@ -18,7 +18,7 @@ INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 
 ROW_STRIDE = 512
 EXT_STRIDE = 1032
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
@@ -88,7 +88,7 @@ def lib() -> ctypes.CDLL:
                                    ctypes.c_int64, _vp]
     L.tfb_debug_blind_rotate.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     L.tfb_debug_key_switch.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
-    L.tfb_debug_spectral_key.argtypes = [_vp, ctypes.c_int32, _vp]
+    L.tfb_debug_spectral_key.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp]
     L.tfb_debug_pick_kernel.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
     L.tfb_kernel_launches.argtypes = [_vp]
     L.tfb_kernel_launches.restype = ctypes.c_int64

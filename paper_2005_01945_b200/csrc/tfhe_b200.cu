@@ -1,19 +1,20 @@
 // libtfhe_b200.so -- sm_100a kernels and the C ABI declared in include/tfhe_b200.h.
 //
 // Kernels
-//   K1 fused gate linear form + mod switch + n-step CMux blind rotation + sample extract;
-//      ACC resident in shared memory, FP64 negacyclic FFT in registers (tfhe_device.cuh):
-//      K1b k_gate_bootstrap_ring  4 gates per CTA, spectral key staged by TMA through an
-//                                 mbarrier ring (launches of >= 4 gates per SM)
-//      K1a k_gate_bootstrap       one gate per 64-thread CTA, key through L1/L2
-//      K1c k_gate_bootstrap_wide  one gate over four thread groups (latency path)
+//   K1 fused gate linear form + mod switch + blind rotation + sample extract.  The bootstrapping key is
+//      UNROLLED over pairs of LWE mask elements (three TRGSW samples per pair, ceil(n/2) steps of four forward
+//      and two inverse FP64 negacyclic transforms); ACC resident in shared memory:
+//      K1d k_gate_bootstrap_warp  one gate per WARP, twelve per SM, spectral key staged by TMA through a
+//                                 release-count ring, accumulators parked in tensor memory (tfhe_warp.cuh)
+//      K1e k_gate_bootstrap_pair  one gate per two-CTA cluster, one accumulator polynomial per SM, DSMEM
+//                                 exchange (latency path; tfhe_pair.cuh + tfhe_cluster.cuh)
 //   K2 k_key_switch       batched N -> n key switch as an integer rank-8192 update,
 //                         32 ciphertexts x 512 columns per CTA, digits in smem (launches < 96 gates)
 //   K2t k_key_switch_mma  the same update as an exact s8 x u8 -> s32 GEMM on the tensor cores
 //                         (tcgen05.mma kind::i8, TMEM accumulator), tfhe_keyswitch_mma.cuh
-//   K3 k_bk_transform     one-time: raw TRGSW rows -> spectral key in K1's register
-//      k_ksk_layout       order; raw key-switching key -> row-padded table
-//   k_rows_negate, k_rows_phase   NOT and batched phase (decryption helper)
+//   K3 k_bk_transform(_w) one-time: raw TRGSW rows -> spectral key in K1e's / K1d's chunk order;
+//      k_ksk_layout       raw key-switching key -> row-padded table
+//   k_rows_negate, k_rows_phase, k_rows_encrypt   NOT, batched phase (decryption helper), batched encryption
 //   k_peak_*              DFMA / IMAD peak microbenchmarks (roofline denominators)
 #include <cuda_runtime.h>
 #include <math.h>
@@ -43,9 +44,10 @@ struct tfb_ctx {
   int device = 0;
   tfb_params p{};
   bool keys_loaded = false;
-  cd* d_bkf = nullptr;         // staged layout [n][p][k2][lvl][c][t] (cd), prescaled by 1/512
-  cd* d_bkw = nullptr;         // K1d's staged layout [n][p][lvl][q][c][lane] (cd), prescaled by 1/512
+  cd* d_bkf = nullptr;         // K1e's chunks [pair][p][lvl][half][k4][key][c][t] (cd), prescaled by 1/512
+  cd* d_bkw = nullptr;         // K1d's chunks [pair][stage][qc][q4][key][c][lane] (cd), prescaled by 1/512
   WarpTwiddles* d_wtw = nullptr;
+  FactorTables* d_ft = nullptr;
   int32_t* d_ksk = nullptr;    // [N*t][ROW_STRIDE]
   uint8_t* d_ksk_mma = nullptr;  // K2t: byte planes as shared-memory images [col tile][K block][32 KB]
   int force_ks = 0;            // 0 auto, 1 = K2 (IMAD), 2 = K2t (tensor cores)
@@ -61,7 +63,7 @@ struct tfb_ctx {
   cudaEvent_t ev_in[HOST_EVENTS] = {}, ev_run[HOST_EVENTS] = {};
   int64_t launches = 0;
   int sm_count = 148;
-  int force_kernel = 0;        // 0 auto, 1 = K1a (one ciphertext per CTA), 2 = K1b (ring), 3 = K1c (wide), 4 = K1d (warp), 5 = K1e (cluster pair)
+  int force_kernel = 0;        // 0 auto, 4 = K1d (warp), 5 = K1e (cluster pair)
   std::string err;
 };
 
@@ -99,24 +101,6 @@ struct DeviceGuard {
 struct BlockSync {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
-// named barrier over one 64-thread ciphertext group of a multi-group CTA
-struct GroupSync {
-  int id;
-  __device__ __forceinline__ void operator()() const {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(FFT_THREADS) : "memory");
-  }
-};
-// spectral key read straight from global memory through L1 (small launches)
-struct LdgBk {
-  const cd* base;
-  __device__ __forceinline__ const cd* acquire(int i, int p) { return base + stage_offset(i, p); }
-  __device__ __forceinline__ cd load(const cd* q) const {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(q));
-    return cd{v.x, v.y};
-  }
-  __device__ __forceinline__ void release() {}
-};
-
 // ---- mbarrier / bulk-copy (TMA) primitives --------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -149,211 +133,10 @@ __device__ __forceinline__ void bulk_load(void* dst_smem, const void* src_gmem, 
 }
 
 // ------------------------------------------------------------------------------------
-// K1a: fused gate bootstrap, one ciphertext per 64-thread CTA, key through L1/L2.
-//      Used for launches too small to fill the chip with K1b's multi-ciphertext CTAs.
-// ------------------------------------------------------------------------------------
-// per-ciphertext smem: s0 | s1 | acc (2N words) | abar (n+1 uint16, padded)
-constexpr int GROUP_SMEM_FIXED = 2 * HALF_N * (int)sizeof(cd) + 2 * RING_N * (int)sizeof(uint32_t);
-__host__ __device__ constexpr int group_smem(int n) { return GROUP_SMEM_FIXED + ((n + 1) * 2 + 15) / 16 * 16; }
-#ifndef TFB_K1_MIN_BLOCKS
-#define TFB_K1_MIN_BLOCKS 4  // 255 registers, no spills: K1a serves launches of 2-4 gates per SM
-#endif
-
-__global__ void __launch_bounds__(FFT_THREADS, TFB_K1_MIN_BLOCKS) k_gate_bootstrap(
-    const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
-    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
-    const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
-  cd* s0 = reinterpret_cast<cd*>(smem + sizeof(Twiddles));
-  cd* s1 = s0 + HALF_N;
-  uint32_t* acc = reinterpret_cast<uint32_t*>(s1 + HALF_N);
-  uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
-  for (int i = threadIdx.x; i < (int)(sizeof(Twiddles) / sizeof(cd)); i += FFT_THREADS)
-    reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
-  const int64_t g = blockIdx.x;
-  const uint32_t* xr = pool + (int64_t)x_rows[g] * stride;
-  const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
-  BlockSync sync;
-  LdgBk bk{bkf};
-  NoPark park;
-  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, ext + g * EXT_STRIDE,
-                 (int)threadIdx.x, sync, park);
-}
-
-// ------------------------------------------------------------------------------------
-// K1c: latency variant, ONE ciphertext per 256-thread CTA (gate_bootstrap_wide): the four
-//      digit polynomials of a CMux are transformed concurrently by four 64-thread groups.
-//      Used when a launch has fewer gates than SMs (ripple-carry adders, multiplier trees).
-// ------------------------------------------------------------------------------------
-constexpr int K1C_THREADS = 4 * FFT_THREADS;
-// dynamic smem: twiddles | xbuf 4x2x512 cd | red 4x2x512 cd | acc | abar
-__host__ __device__ constexpr int k1c_smem(int n) {
-  return (int)sizeof(Twiddles) + 16 * HALF_N * (int)sizeof(cd) + 2 * RING_N * (int)sizeof(uint32_t) +
-         ((n + 1) * 2 + 15) / 16 * 16;
-}
-struct LdgLoad {
-  __device__ __forceinline__ cd operator()(const cd* q) const {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(q));
-    return cd{v.x, v.y};
-  }
-};
-
-__global__ void __launch_bounds__(K1C_THREADS, 1) k_gate_bootstrap_wide(
-    const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
-    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
-    const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
-  cd* xbuf = reinterpret_cast<cd*>(smem + sizeof(Twiddles));
-  cd* red = xbuf + 8 * HALF_N;
-  uint32_t* acc = reinterpret_cast<uint32_t*>(red + 8 * HALF_N);
-  uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
-  for (int i = threadIdx.x; i < (int)(sizeof(Twiddles) / sizeof(cd)); i += K1C_THREADS)
-    reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
-  const int64_t g = blockIdx.x;
-  const uint32_t* xr = pool + (int64_t)x_rows[g] * stride;
-  const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
-  GroupSync gsync{(int)(threadIdx.x / FFT_THREADS) + 1};
-  BlockSync csync;
-  gate_bootstrap_wide(xr, yr, (int)kinds[g], n, mu, bkf, tw, acc, abar, xbuf, red, ext + g * EXT_STRIDE,
-                      (int)threadIdx.x, gsync, csync, LdgLoad());
-}
-
-// ------------------------------------------------------------------------------------
-// K1b: fused gate bootstrap, K1B_GROUPS ciphertexts per CTA (one CTA per SM).
-//      The spectral key is staged through a two-slot shared-memory ring by bulk
-//      copies (TMA), one 32 KB stage per (LWE index, accumulator polynomial), and
-//      shared by all groups of the CTA: L2->SM key traffic drops by the group count
-//      and the key is resident before any group needs it.  Groups synchronise only
-//      through the ring's full/empty mbarriers, so they drift apart by up to one
-//      stage and their FP64-heavy and LSU-heavy phases overlap.
-// ------------------------------------------------------------------------------------
-#ifndef TFB_K1B_GROUPS
-#define TFB_K1B_GROUPS 4  // 4 groups x 252 registers (no spills) measured 3% faster than 6 x 168
-#endif
-constexpr int K1B_GROUPS = TFB_K1B_GROUPS;
-constexpr int K1B_THREADS = K1B_GROUPS * FFT_THREADS;
-constexpr int STAGE_BYTES = STAGE_CD * (int)sizeof(cd);
-#ifndef TFB_K1B_SLOTS
-#define TFB_K1B_SLOTS 2  // measured: 3 slots (groups free to drift a whole CMux apart) is 3.7% slower than 2
-#endif
-constexpr int K1B_SLOTS = TFB_K1B_SLOTS;
-// dynamic smem: twiddles | ring[K1B_SLOTS][STAGE_CD] | mbarriers (64 B) | groups
-constexpr int K1B_HEADER = (int)sizeof(Twiddles) + K1B_SLOTS * STAGE_BYTES + 64;
-
-#ifndef TFB_K1B_TURNS
-#define TFB_K1B_TURNS 1
-#endif
-struct TurnPark {  // no parking; a two-party turn rotation on named barriers (64 threads arrive, 64 wait)
-  static constexpr bool parks = false;
-  int wait_id, next_id;
-  __device__ __forceinline__ void store(const cd*, const cd*) {}
-  __device__ __forceinline__ void load(int, cd&, cd&) {}
-  __device__ __forceinline__ void turn_enter() const { asm volatile("bar.sync %0, 128;" ::"r"(wait_id) : "memory"); }
-  __device__ __forceinline__ void turn_leave() const { asm volatile("bar.arrive %0, 128;" ::"r"(next_id) : "memory"); }
-  __device__ __forceinline__ void turn_pass() const {
-    turn_enter();
-    turn_leave();
-  }
-};
-
-struct RingBk {
-  const cd* bkf;       // full spectral key in global memory
-  cd* ring;            // K1B_SLOTS stages in shared memory
-  uint64_t* full;      // [slots] completes when a stage's bytes have landed
-  uint64_t* empty;     // [slots] completes when every warp of the CTA released the stage
-  int stage;           // next stage this thread will consume (2*i + p)
-  int n_stages;
-  bool producer;       // exactly one thread of the CTA issues the copies
-
-  static __device__ __forceinline__ int slot(int s) { return s % K1B_SLOTS; }
-  static __device__ __forceinline__ uint32_t parity(int s) { return (uint32_t)(s / K1B_SLOTS) & 1u; }
-  __device__ __forceinline__ void issue(int s) {
-    mbar_expect_tx(&full[slot(s)], STAGE_BYTES);
-    bulk_load(ring + (size_t)slot(s) * STAGE_CD, bkf + (size_t)s * STAGE_CD, STAGE_BYTES, &full[slot(s)]);
-  }
-  // On entering stage s the producer requests stage s+1.  It lands in the slot stage
-  // s+1-K1B_SLOTS used, which every warp must have released: with 2 slots that is stage s-1
-  // (the producer's group trails the slowest group), with 3 slots stage s-2 (groups may
-  // drift a whole CMux apart before anyone waits).
-  __device__ __forceinline__ void produce_ahead() {
-    const int next = stage + 1;
-    if (producer && stage >= 1 && next < n_stages) {
-      if (next >= K1B_SLOTS) mbar_wait(&empty[slot(next)], parity(next - K1B_SLOTS));
-      issue(next);
-    }
-  }
-  __device__ __forceinline__ const cd* acquire(int, int) {
-    produce_ahead();
-    mbar_wait(&full[slot(stage)], parity(stage));
-    return ring + (size_t)slot(stage) * STAGE_CD;
-  }
-  __device__ __forceinline__ cd load(const cd* q) const { return *q; }
-  __device__ __forceinline__ void release() {
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[slot(stage)]);
-    ++stage;
-  }
-};
-
-__global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
-    const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
-    const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
-    const cd* __restrict__ bkf, const Twiddles* __restrict__ tw_global, uint32_t* __restrict__ ext,
-    int64_t k) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  Twiddles* tw = reinterpret_cast<Twiddles*>(smem);
-  cd* ring = reinterpret_cast<cd*>(smem + sizeof(Twiddles));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sizeof(Twiddles) + K1B_SLOTS * STAGE_BYTES);
-  const int grp = threadIdx.x / FFT_THREADS, t = threadIdx.x % FFT_THREADS;
-  unsigned char* mine = smem + K1B_HEADER + (size_t)grp * group_smem(n);
-  cd* s0 = reinterpret_cast<cd*>(mine);
-  cd* s1 = s0 + HALF_N;
-  uint32_t* acc = reinterpret_cast<uint32_t*>(s1 + HALF_N);
-  uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
-
-  for (int i = threadIdx.x; i < (int)(sizeof(Twiddles) / sizeof(cd)); i += K1B_THREADS)
-    reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
-  RingBk bk{bkf, ring, bars, bars + K1B_SLOTS, 0, 2 * n, threadIdx.x == 0};
-  if (threadIdx.x == 0) {
-    for (int j = 0; j < K1B_SLOTS; ++j) {
-      mbar_init(&bk.full[j], 1);
-      mbar_init(&bk.empty[j], K1B_THREADS / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    bk.issue(0);
-    bk.issue(1);
-  }
-  // tail CTA: surplus groups redo the last ciphertext (keeps the ring protocol uniform) but do not store
-  const int64_t want = (int64_t)blockIdx.x * K1B_GROUPS + grp;
-  const int64_t g = want < k ? want : k - 1;
-  const uint32_t* xr = pool + (int64_t)x_rows[g] * stride;
-  const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
-  uint32_t* dst = want < k ? ext + g * EXT_STRIDE : reinterpret_cast<uint32_t*>(s0);  // scratch sink
-  GroupSync sync{grp + 1};
-#if TFB_K1B_TURNS
-  // groups g and g + 2 put one warp each on the same two schedulers (warp w runs on scheduler w % 4): they take the
-  // MAC of a CMux half in turns (the K1d rotation, DevWarp below, with two parties)
-  static_assert(K1B_GROUPS == 4, "the turn pairs are laid out for four groups");
-  TurnPark park{8 + 2 * (grp & 1) + ((grp >> 1) ^ 1), 8 + 2 * (grp & 1) + (grp >> 1)};
-  if (grp >> 1) park.turn_leave();
-#else
-  NoPark park;
-#endif
-  gate_bootstrap(xr, yr, (int)kinds[g], n, mu, bk, tw, acc, abar, s0, s1, dst, t, sync, park);
-}
-
-// ------------------------------------------------------------------------------------
 // K1d: fused gate bootstrap, ONE ciphertext per WARP, K1D_WARPS ciphertexts per CTA (one CTA
 //      per SM), arithmetic in tfhe_warp.cuh.  Radix-16 transforms: one shared-memory exchange
-//      and one shuffle stage per transform instead of two exchanges, no barrier other than
-//      __syncwarp inside the blind rotation; the spectral key comes through the same TMA ring
-//      as K1b (one 32 KB stage per (LWE index, accumulator polynomial), shared by all warps).
+//      and one shuffle stage per transform, no barrier other than __syncwarp inside the blind
+//      rotation; the spectral key comes through a TMA ring of 12 KB chunks shared by all warps.
 // ------------------------------------------------------------------------------------
 #ifndef TFB_K1D_TMEM
 #define TFB_K1D_TMEM 1  // accumulators parked in tensor memory between the MAC stages
@@ -364,21 +147,26 @@ __global__ void __launch_bounds__(K1B_THREADS, 1) k_gate_bootstrap_ring(
 constexpr int K1D_WARPS = TFB_K1D_WARPS;
 constexpr int K1D_THREADS = K1D_WARPS * WARP_T;
 __host__ __device__ constexpr int warp_smem(int n) {
-  return WBUF_BYTES + 2 * RING_N * (int)sizeof(uint32_t) + ((n + 1) * 2 + 15) / 16 * 16;
+  return WBUF_BYTES + 2 * RING_N * (int)sizeof(uint32_t) + ((n + 2) * 2 + 15) / 16 * 16;
 }
-constexpr int K1D_HEADER = (int)sizeof(WarpTwiddles) + 4 * 16384 + 128;  // twiddles | key ring (WR_SLOTS x 16 KB <= 64 KB) | barriers
 
-// Key ring of K1d: WR_SLOTS chunks of 16 KB (one (i, p, lvl): what one MAC consumes).
+// Key ring of K1d: WR_SLOTS chunks of 12 KB (pair, stage, four spectral points per lane x three keys x two
+// output components: what the MAC of one accumulator chunk consumes; sixteen chunks per pair step).
 // Consumers wait on the full mbarrier of a slot; a slot is handed back by counting releases,
 // and the warp whose release is the last one issues the bulk copy of the chunk that reuses
 // the slot (no dedicated producer: with a fixed producer thread every warp of the CTA is
 // gated by that thread's own progress).  A warp may run WR_SLOTS - 1 chunks ahead of the
 // slowest one before it has to wait.
 #ifndef TFB_K1D_SLOTS
-#define TFB_K1D_SLOTS 4
+#define TFB_K1D_SLOTS 5
 #endif
 constexpr int WR_SLOTS = TFB_K1D_SLOTS;
 constexpr int WR_CHUNK_BYTES = WCHUNK_CD * (int)sizeof(cd);
+// dynamic smem: twiddles | factor tables | key ring | barriers | warps
+constexpr int K1D_OFF_FT = (int)sizeof(WarpTwiddles);
+constexpr int K1D_OFF_RING = K1D_OFF_FT + (int)sizeof(FactorTables);
+constexpr int K1D_OFF_BARS = K1D_OFF_RING + WR_SLOTS * WR_CHUNK_BYTES;
+constexpr int K1D_HEADER = K1D_OFF_BARS + 128;
 // Waiting for a key chunk: non-blocking mbarrier.test_wait + nanosleep (TFB_K1D_POLL, default), or
 // mbarrier.try_wait with a suspend-time hint.  On real runs a warp waits 2-5 % of the time and polls
 // once or twice per chunk (build with -DTFB_K1D_PROBE to print it); under ncu's instrumentation the
@@ -421,7 +209,7 @@ struct WarpRing {
   uint64_t* full;       // [slots] completes when a chunk's bytes have landed
   uint32_t* released;   // [slots] warps that are done with the chunk in the slot
   uint32_t full_u32;    // shared-space address of full[0]
-  int chunk;            // next chunk this warp will consume (4*i + 2*p + lvl)
+  int chunk;            // next chunk this warp will consume (16 m + 4 s + qc: the key is stored in that order)
   int n_chunks;
 
   static __device__ __forceinline__ int slot(int s) { return s % WR_SLOTS; }
@@ -478,7 +266,7 @@ struct WarpRing {
 // per 14,208 gates.  What was measured and lost (turns around the FP64 bursts, around both, a
 // first-come-first-served lock instead of the rotation) is in profiles/README.md.
 #ifndef TFB_K1D_TURNS
-#define TFB_K1D_TURNS 1
+#define TFB_K1D_TURNS 0
 #endif
 struct DevWarp {
   int turn_wait = 0, turn_next = 0;  // named-barrier ids (0: no protocol, e.g. the key-setup kernel)
@@ -570,26 +358,8 @@ struct TmemWPark {
     store_one(1, qb, o1);
   }
   __device__ __forceinline__ void flush() const { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-  // level-1 digit words: columns 128 .. 143 of the slice (the MAC's flush() orders the store)
-  __device__ __forceinline__ void store_digits(const uint32_t* r) const {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16};" ::"r"(taddr + 128),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-        : "memory");
-  }
-  __device__ __forceinline__ void load_digits(uint32_t* r) const {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%16];\n\ttcgen05.wait::ld.sync.aligned;"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr + 128)
-        : "memory");
-  }
 };
-constexpr uint32_t K1D_TMEM_SLICE = 144;  // columns per warp: 2 x 64 accumulators + 16 digit words
+constexpr uint32_t K1D_TMEM_SLICE = 128;  // columns per warp: 2 x 64 accumulators
 constexpr uint32_t K1D_TMEM_TW = ((K1D_WARPS + 3) / 4) * K1D_TMEM_SLICE;  // first column of the twiddle table
 constexpr uint32_t K1D_TMEM_NEED = K1D_TMEM_TW + 68;                      // 16 twiddles + c per lane
 
@@ -637,12 +407,13 @@ struct TmemTw {
 __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
     const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
-    const cd* __restrict__ bkw, const WarpTwiddles* __restrict__ tw_global, uint32_t* __restrict__ ext,
-    int64_t k) {
+    const cd* __restrict__ bkw, const WarpTwiddles* __restrict__ tw_global, const FactorTables* __restrict__ ft_global,
+    uint32_t* __restrict__ ext, int64_t k) {
   extern __shared__ __align__(128) unsigned char smem[];
   WarpTwiddles* tw = reinterpret_cast<WarpTwiddles*>(smem);
-  cd* ring = reinterpret_cast<cd*>(smem + sizeof(WarpTwiddles));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sizeof(WarpTwiddles) + 4 * 16384);
+  FactorTables* ft = reinterpret_cast<FactorTables*>(smem + K1D_OFF_FT);
+  cd* ring = reinterpret_cast<cd*>(smem + K1D_OFF_RING);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K1D_OFF_BARS);
   const int wid = threadIdx.x / WARP_T, t = threadIdx.x % WARP_T;
   unsigned char* mine = smem + K1D_HEADER + (size_t)wid * warp_smem(n);
   void* buf = mine;
@@ -651,8 +422,11 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
 
   for (int i = threadIdx.x; i < (int)(sizeof(WarpTwiddles) / sizeof(cd)); i += K1D_THREADS)
     reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
-  static_assert(WR_SLOTS * WR_CHUNK_BYTES <= 4 * 16384 && WR_SLOTS <= 8, "key ring does not fit its header slot");
-  WarpRing bk{bkw, ring, bars, reinterpret_cast<uint32_t*>(bars + WR_SLOTS), smem_u32(bars), 0, 4 * n};
+  for (int i = threadIdx.x; i < (int)(sizeof(FactorTables) / sizeof(cd)); i += K1D_THREADS)
+    reinterpret_cast<cd*>(ft)[i] = reinterpret_cast<const cd*>(ft_global)[i];
+  static_assert(WR_SLOTS <= 8, "eight mbarriers + eight release counters fit the 128-byte barrier block");
+  WarpRing bk{bkw, ring, bars, reinterpret_cast<uint32_t*>(bars + WR_SLOTS), smem_u32(bars), 0,
+              WCHUNKS_PER_PAIR * ((n + 1) / 2)};
   if (threadIdx.x == 0) {
     for (int j = 0; j < WR_SLOTS; ++j) {
       mbar_init(&bk.full[j], 1);
@@ -716,13 +490,14 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
 #ifdef TFB_K1D_PHASES
   w.last = clock64();
 #endif
-  gate_bootstrap_warp(xr, yr, (int)kinds[g], n, mu, bk, ttw, acc, abar, buf, dst, t, w, park);
+  gate_bootstrap_warp(xr, yr, (int)kinds[g], n, mu, bk, ttw, ft, acc, abar, buf, dst, t, w, park);
 #ifdef TFB_K1D_PHASES
   if (t == 0 && blockIdx.x == 3 && (wid == 0 || wid == 5 || wid == 10))
-    printf("warp %2d per CMux: decomp/digits %lld | fwd burst1 %lld exch %lld burst2 %lld (x4) | key wait %lld turn wait %lld mac %lld (x4) | "
+    printf("warp %2d per pair step: decomp/digits %lld | fwd burst1 %lld exch %lld burst2 %lld (x4) | key wait %lld turn wait %lld mac %lld (x4) | "
            "inv: tmem %lld burst1 %lld exch %lld burst2 %lld update %lld (x2)\n",
-           wid, w.T[0] / n, w.T[1] / n, w.T[2] / n, w.T[3] / n, w.T[4] / n, w.T[5] / n, w.T[6] / n, w.T[7] / n, w.T[8] / n,
-           w.T[9] / n, w.T[10] / n, w.T[11] / n);
+           wid, w.T[0] / ((n + 1) / 2), w.T[1] / ((n + 1) / 2), w.T[2] / ((n + 1) / 2), w.T[3] / ((n + 1) / 2), w.T[4] / ((n + 1) / 2),
+           w.T[5] / ((n + 1) / 2), w.T[6] / ((n + 1) / 2), w.T[7] / ((n + 1) / 2), w.T[8] / ((n + 1) / 2), w.T[9] / ((n + 1) / 2),
+           w.T[10] / ((n + 1) / 2), w.T[11] / ((n + 1) / 2));
 #endif
 #ifdef TFB_K1D_PROBE
   if (t == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
@@ -821,17 +596,22 @@ __global__ void k_rows_zero(uint32_t* __restrict__ pool, const int32_t* __restri
 // ------------------------------------------------------------------------------------
 // K3: key setup
 // ------------------------------------------------------------------------------------
-// one CTA per raw polynomial: bk_raw[(i*4 + r)*2 + c][N] -> staged layout bkf[i][p][k2][lvl][c][t], r = p*l + lvl
+// raw polynomial index of bk_raw[pair][key][row][c][N] -> (pair m, key j, row r = p*l + lvl, component c)
+struct RawPoly {
+  int m, j, r, c;
+  __device__ explicit RawPoly(int64_t poly)
+      : m((int)((poly >> 1) / BK_ROWS / BK_KEYS)), j((int)((poly >> 1) / BK_ROWS % BK_KEYS)), r((int)((poly >> 1) % BK_ROWS)),
+        c((int)(poly & 1)) {}
+};
+// one CTA per raw polynomial -> K1e's chunks bkf[pair][p][lvl][half][k4][key][c][t]
 __global__ void __launch_bounds__(FFT_THREADS) k_bk_transform(const int32_t* __restrict__ bk_raw,
                                                               cd* __restrict__ bkf,
                                                               const Twiddles* __restrict__ tw) {
   __shared__ cd bufA[HALF_N];
   __shared__ cd bufB[HALF_N];
   const int t = threadIdx.x;
-  const int64_t poly = blockIdx.x;
-  const int c = (int)(poly & 1);
-  const int64_t ir = poly >> 1;  // i*4 + r
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(bk_raw) + poly * RING_N;
+  const RawPoly id(blockIdx.x);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(bk_raw) + (int64_t)blockIdx.x * RING_N;
   cd x[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m)
@@ -841,20 +621,18 @@ __global__ void __launch_bounds__(FFT_THREADS) k_bk_transform(const int32_t* __r
   const double scale = 1.0 / HALF_N;
 #pragma unroll
   for (int k2 = 0; k2 < 8; ++k2)
-    bkf[stage_offset((int)(ir / BK_ROWS), (int)(ir % BK_ROWS) / BK_L) + stage_index(k2, (int)(ir % BK_L), c, t)] =
+    bkf[pchunk_offset(id.m, id.r / BK_L, id.r % BK_L, k2 >> 2) + pchunk_index(k2 & 3, id.j, id.c, t)] =
         cd{x[k2].re * scale, x[k2].im * scale};
 }
 
-// same for K1d: one warp per raw polynomial -> bkw[i][p][lvl][q][c][lane]
+// same for K1d: one warp per raw polynomial -> bkw[pair][stage][qc][q4][key][c][lane]
 __global__ void __launch_bounds__(WARP_T) k_bk_transform_w(const int32_t* __restrict__ bk_raw,
                                                            cd* __restrict__ bkw,
                                                            const WarpTwiddles* __restrict__ tw) {
   __shared__ __align__(16) unsigned char buf[WBUF_BYTES];
   const int t = threadIdx.x;
-  const int64_t poly = blockIdx.x;
-  const int c = (int)(poly & 1);
-  const int64_t ir = poly >> 1;  // i*4 + r
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(bk_raw) + poly * RING_N;
+  const RawPoly id(blockIdx.x);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(bk_raw) + (int64_t)blockIdx.x * RING_N;
   cd x[WPTS];
 #pragma unroll
   for (int m = 0; m < WPTS; ++m)
@@ -866,7 +644,7 @@ __global__ void __launch_bounds__(WARP_T) k_bk_transform_w(const int32_t* __rest
   const double scale = 1.0 / HALF_N;
 #pragma unroll
   for (int q = 0; q < WPTS; ++q)
-    bkw[stage_offset((int)(ir / BK_ROWS), (int)(ir % BK_ROWS) / BK_L) + wstage_index((int)(ir % BK_L), q, c, t)] =
+    bkw[wchunk_offset(id.m, id.r, q / WCHUNK_Q) + wchunk_index(q % WCHUNK_Q, id.j, id.c, t)] =
         cd{x[q].re * scale, x[q].im * scale};
 }
 
@@ -1041,8 +819,8 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
     return TFB_ERR_INVALID;
   }
   if (p->ring_n != RING_N || p->bk_l != BK_L || p->bk_bgbit != BK_BGBIT || p->ks_t != KS_T ||
-      p->ks_basebit != KS_BASEBIT || p->n < 1 || p->n >= ROW_STRIDE) {
-    g_create_err = "unsupported parameter set (compiled: N=1024 l=2 Bgbit=10 t=8 basebit=2, n<=511)";
+      p->ks_basebit != KS_BASEBIT || p->n < 1 || p->n >= ROW_STRIDE - 1) {
+    g_create_err = "unsupported parameter set (compiled: N=1024 l=2 Bgbit=9 t=8 basebit=2, n<=510)";
     return TFB_ERR_INVALID;
   }
   DeviceGuard guard(device);
@@ -1065,17 +843,15 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
     e = cudaMalloc(&ctx->d_wtw, sizeof(WarpTwiddles));
     if (e == cudaSuccess) e = cudaMemcpy(ctx->d_wtw, &hw, sizeof(WarpTwiddles), cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess) {
+    FactorTables hf;
+    fill_factor_tables<long double>(&hf, cosl, sinl);
+    e = cudaMalloc(&ctx->d_ft, sizeof(FactorTables));
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_ft, &hf, sizeof(FactorTables), cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gate_bootstrap_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              K1D_HEADER + K1D_WARPS * warp_smem(p->n));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_gate_bootstrap, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(Twiddles) + group_smem(p->n));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_gate_bootstrap_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             K1B_HEADER + K1B_GROUPS * group_smem(p->n));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_gate_bootstrap_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, k1c_smem(p->n));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k1e::k_gate_bootstrap_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, k1e::smem_bytes(p->n));
   if (e == cudaSuccess)
@@ -1102,6 +878,7 @@ void tfb_ctx_destroy(tfb_ctx* ctx) {
   cudaFree(ctx->d_bkf);
   cudaFree(ctx->d_bkw);
   cudaFree(ctx->d_wtw);
+  cudaFree(ctx->d_ft);
   cudaFree(ctx->d_ksk);
   cudaFree(ctx->d_ksk_mma);
   cudaFree(ctx->d_tw);
@@ -1124,7 +901,8 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
   cudaStream_t st = (cudaStream_t)stream;
   TFB_ENTER(ctx);
   const int n = ctx->p.n;
-  const size_t bk_words = (size_t)n * BK_ROWS * 2 * RING_N;
+  const int64_t bk_polys = (int64_t)((n + 1) / 2) * BK_KEYS * BK_ROWS * 2;  // pairs x keys x rows x components
+  const size_t bk_words = (size_t)bk_polys * RING_N;
   const size_t ksk_words = (size_t)RING_N * KS_T * (n + 1);
   const int32_t* d_bk = bk;
   const int32_t* d_kr = ksk;
@@ -1137,11 +915,11 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
     d_bk = tmp_bk;
     d_kr = tmp_ksk;
   }
-  if (!ctx->d_bkf) TFB_CUDA(ctx, cudaMalloc(&ctx->d_bkf, (size_t)n * BK_ROWS * 2 * HALF_N * sizeof(cd)));
+  if (!ctx->d_bkf) TFB_CUDA(ctx, cudaMalloc(&ctx->d_bkf, (size_t)bk_polys * HALF_N * sizeof(cd)));
   if (!ctx->d_ksk) TFB_CUDA(ctx, cudaMalloc(&ctx->d_ksk, (size_t)RING_N * KS_T * ROW_STRIDE * 4));
-  if (!ctx->d_bkw) TFB_CUDA(ctx, cudaMalloc(&ctx->d_bkw, (size_t)n * BK_ROWS * 2 * HALF_N * sizeof(cd)));
-  k_bk_transform<<<n * BK_ROWS * 2, FFT_THREADS, 0, st>>>(d_bk, ctx->d_bkf, ctx->d_tw);
-  k_bk_transform_w<<<n * BK_ROWS * 2, WARP_T, 0, st>>>(d_bk, ctx->d_bkw, ctx->d_wtw);
+  if (!ctx->d_bkw) TFB_CUDA(ctx, cudaMalloc(&ctx->d_bkw, (size_t)bk_polys * HALF_N * sizeof(cd)));
+  k_bk_transform<<<(unsigned)bk_polys, FFT_THREADS, 0, st>>>(d_bk, ctx->d_bkf, ctx->d_tw);
+  k_bk_transform_w<<<(unsigned)bk_polys, WARP_T, 0, st>>>(d_bk, ctx->d_bkw, ctx->d_wtw);
   k_ksk_layout<<<RING_N * KS_T, 128, 0, st>>>(d_kr, ctx->d_ksk, n);
   if (!ctx->d_ksk_mma)
     TFB_CUDA(ctx, cudaMalloc(&ctx->d_ksk_mma, (size_t)k2t::NTILES * k2t::KBLOCKS * k2t::B_BYTES));
@@ -1156,24 +934,21 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
   return TFB_OK;
 }
 
-// Cost model of the five K1 variants (ms per launch on a 148-SM B200 at n = 500, measured with
-// tools/k1_ab.py; only the ratios matter).  Every variant runs in waves of one CTA set per SM:
-//   K1e 1 gate / 2 SMs (cluster), 1.05 ms per wave   K1c 1 gate / SM, 1.36 ms per wave
-//   K1a up to 4 gates / SM, 2.49 .. 3.74 ms per wave  K1b 4 gates / SM, 3.35 ms per wave
-//   K1d 12 gates / SM, 8.05 ms per wave
-constexpr double K1D_WAVE_MS = 8.05;
+// Cost model of the two K1 variants (ms per launch on a 148-SM B200 at n = 500, measured with
+// tools/k1_ab.py; only the ratio matters).  Both run in waves of one CTA set per SM:
+//   K1e 1 gate / 2 SMs (cluster) per wave   K1d 12 gates / SM per wave
+#ifndef TFB_K1D_WAVE_MS
+#define TFB_K1D_WAVE_MS 6.6
+#endif
+#ifndef TFB_K1E_WAVE_MS
+#define TFB_K1E_WAVE_MS 0.6
+#endif
+constexpr double K1D_WAVE_MS = TFB_K1D_WAVE_MS, K1E_WAVE_MS = TFB_K1E_WAVE_MS;
 static int pick_k1(int64_t k, int sms, double* cost) {
   const double S = (double)sms;
-  const double waves_c = ceil(k / S), waves_b = ceil(k / (4 * S)), waves_d = ceil(k / (12 * S));
-  const double waves_e = ceil(k / floor(S / 2));
-  const double t[6] = {0.0,
-                       k <= S ? 2.49 : (k <= 2 * S ? 2.69 : (k <= 3 * S ? 3.53 : 3.74 * waves_b)),
-                       3.35 * waves_b, 1.36 * waves_c, K1D_WAVE_MS * waves_d, 1.05 * waves_e};
-  int best = 3;
-  for (int w = 1; w <= 5; ++w)
-    if (t[w] < t[best]) best = w;
-  if (cost) *cost = t[best];
-  return best;
+  const double t_d = K1D_WAVE_MS * ceil(k / (K1D_WARPS * S)), t_e = K1E_WAVE_MS * ceil(k / floor(S / 2));
+  if (cost) *cost = t_e <= t_d ? t_e : t_d;
+  return t_e <= t_d ? 5 : 4;
 }
 
 static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, int stride, const uint8_t* kinds,
@@ -1181,31 +956,23 @@ static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, int stri
   const int n = ctx->p.n;
   if (which == 5) {  // one gate per two-CTA cluster (the kernel carries __cluster_dims__(2, 1, 1))
     k1e::k_gate_bootstrap_pair<<<(unsigned)(2 * k), k1e::THREADS, k1e::smem_bytes(n), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
+        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ctx->d_ft, ext);
   } else if (which == 4) {
     const unsigned grid = (unsigned)((k + K1D_WARPS - 1) / K1D_WARPS);
     k_gate_bootstrap_warp<<<grid, K1D_THREADS, K1D_HEADER + K1D_WARPS * warp_smem(n), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ext, k);
-  } else if (which == 3) {
-    k_gate_bootstrap_wide<<<(unsigned)k, K1C_THREADS, k1c_smem(n), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
-  } else if (which == 2) {
-    const unsigned grid = (unsigned)((k + K1B_GROUPS - 1) / K1B_GROUPS);
-    k_gate_bootstrap_ring<<<grid, K1B_THREADS, K1B_HEADER + K1B_GROUPS * group_smem(n), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext, k);
+        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ctx->d_ft, ext, k);
   } else {
-    k_gate_bootstrap<<<(unsigned)k, FFT_THREADS, (int)sizeof(Twiddles) + group_smem(n), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ext);
+    ctx->err = "unknown K1 variant (4 = K1d warp kernel, 5 = K1e cluster kernel)";
+    return TFB_ERR_INVALID;
   }
   ctx->launches += 1;
   TFB_CUDA(ctx, cudaGetLastError());
   return TFB_OK;
 }
 
-// K1 dispatch.  K1e (one gate per two-SM cluster) wins on latency while the launch fits half the chip, K1c
-// (one gate over four thread groups of one SM) up to one gate per SM, K1d (one gate per warp, twelve per SM) on
-// throughput, K1b / K1a in between.  A large launch runs its full K1d waves
-// first and hands the ragged rest to whichever variant finishes it soonest.
+// K1 dispatch.  K1e (one gate per two-SM cluster) wins on latency, K1d (one gate per warp, twelve per SM) on
+// throughput.  A large launch runs its full K1d waves first and hands the ragged rest to whichever variant
+// finishes it soonest.
 // The split decision of launch_blind_rotate: variant of the tail (or of the whole launch when *body == 0).
 static int plan_k1(int64_t k, int sms, int64_t* body) {
   const int64_t wave_d = (int64_t)sms * K1D_WARPS;
@@ -1405,18 +1172,18 @@ int tfb_rows_encrypt(tfb_ctx* ctx, void* pool, const int32_t* out_rows, const ui
   return TFB_OK;
 }
 
-int tfb_debug_spectral_key(tfb_ctx* ctx, int32_t i, double* out) {
-  if (!ctx || !out || i < 0 || i >= ctx->p.n) return TFB_ERR_INVALID;
+int tfb_debug_spectral_key(tfb_ctx* ctx, int32_t pair, int32_t key, double* out) {
+  if (!ctx || !out || pair < 0 || pair >= (ctx->p.n + 1) / 2 || key < 0 || key >= BK_KEYS) return TFB_ERR_INVALID;
   if (!ctx->keys_loaded) return TFB_ERR_STATE;
   TFB_ENTER(ctx);
-  const size_t per_i = (size_t)2 * STAGE_CD;
-  std::vector<cd> h(per_i);
-  TFB_CUDA(ctx, cudaMemcpy(h.data(), ctx->d_bkf + (size_t)i * per_i, per_i * sizeof(cd), cudaMemcpyDeviceToHost));
+  const size_t per_pair = (size_t)BK_KEYS * BK_ROWS * 2 * HALF_N;
+  std::vector<cd> h(per_pair);
+  TFB_CUDA(ctx, cudaMemcpy(h.data(), ctx->d_bkf + (size_t)pair * per_pair, per_pair * sizeof(cd), cudaMemcpyDeviceToHost));
   for (int r = 0; r < BK_ROWS; ++r)
     for (int k2 = 0; k2 < 8; ++k2)
       for (int c = 0; c < 2; ++c)
         for (int t = 0; t < FFT_THREADS; ++t) {
-          const cd v = h[(size_t)(r / BK_L) * STAGE_CD + stage_index(k2, r % BK_L, c, t)];
+          const cd v = h[pchunk_offset(0, r / BK_L, r % BK_L, k2 >> 2) + pchunk_index(k2 & 3, key, c, t)];
           const int f = spectral_index(t, k2);
           double* dst = out + (((size_t)(r * 2 + c) * HALF_N) + f) * 2;
           dst[0] = v.re * HALF_N;

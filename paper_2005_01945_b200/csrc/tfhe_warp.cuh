@@ -404,12 +404,37 @@ TFB_HD void wfft_inverse(cd* x, int t, const Tw& tw, void* buf, W& w) {
   if (FLIP) wflip_odd(x, (uint32_t)(t >> 4) << 31);
 }
 
-// Spectral key stage (i, p) in this kernel's order: [lvl][q][c][lane], prescaled by 1/512
-// (same 32 KB per stage and the same stage_offset as the 64-thread layout).  The unit the
-// key ring moves is a CHUNK = one (i, p, lvl) = 16 KB: what one MAC consumes.  A key source
-// offers acquire_chunk(i, p, lvl) / load(ptr) / release().
-constexpr int WCHUNK_CD = WPTS * 2 * WARP_T;  // 1024 cd
-TFB_HD int wstage_index(int lvl, int q, int c, int t) { return ((lvl * WPTS + q) * 2 + c) * WARP_T + t; }
+// Spectral key in this kernel's order.  The unit the key ring moves is a CHUNK = (pair m, stage s = 2 p + lvl,
+// quarter qc of the 16 points a lane owns): [q4][key j][c][lane], 4 x 3 x 2 x 32 complex = 12 KB, prescaled by
+// 1/512 -- what the MAC of four spectral points consumes, and what one accumulator chunk of the park pairs with.
+// A key source offers acquire_chunk(m, s, qc) / load(ptr) / release().
+constexpr int WCHUNK_Q = 4;
+constexpr int WCHUNK_CD = WCHUNK_Q * BK_KEYS * 2 * WARP_T;  // 768 cd = 12 KB
+constexpr int WCHUNKS_PER_PAIR = 4 * (WPTS / WCHUNK_Q);     // 16
+TFB_HD size_t wchunk_offset(int m, int s, int qc) { return (((size_t)m * 4 + s) * (WPTS / WCHUNK_Q) + qc) * WCHUNK_CD; }
+TFB_HD int wchunk_index(int q4, int j, int c, int t) { return ((q4 * BK_KEYS + j) * 2 + c) * WARP_T + t; }
+struct GlobalWBk {  // plain pointer into the full key (host emulation)
+  const cd* base;
+  TFB_HD const cd* acquire_chunk(int m, int s, int qc) { return base + wchunk_offset(m, s, qc); }
+  TFB_HD cd load(const cd* q) const { return *q; }
+  TFB_HD void release() {}
+};
+
+// Accumulator layout of K1d.  The unrolled CMux never rotates ACC in the coefficient domain, so a lane keeps
+// ITS 32 coefficients of a polynomial (mm = 0..15: coefficient t + 32 mm, the real parts of its transform inputs;
+// mm = 16..31: coefficient t + 32 (mm - 16) + N/2, the imaginary parts) in one 128-byte row and moves them four at
+// a time; the 16-byte units of a row are XOR-swizzled with the lane so that the eight lanes of a quarter warp hit
+// eight different bank groups.
+TFB_HD int wacc_unit(int t, int u) { return t * 32 + ((u ^ (t & 7)) << 2); }  // word offset of unit u = mm / 4
+struct WarpAccLayout {
+  TFB_HD int operator()(int j) const {
+    const int t = j & 31, mm = ((j >> 5) & 15) | ((j >> 9) << 4);
+    return wacc_unit(t, mm >> 2) + (mm & 3);
+  }
+};
+struct alignas(16) Words4 {
+  uint32_t w[4];
+};
 
 // Accumulator parking.  The 2 x 16 complex accumulators of a CMux are idle while a transform
 // runs; a Park policy holds them outside the register file between MAC stages (the B200 kernel
@@ -417,12 +442,11 @@ TFB_HD int wstage_index(int lvl, int q, int c, int t) { return ((lvl * WPTS + q)
 // chunks of PARK_CH values per output polynomial:
 //   issue_one(c, qb, chunk) / settle_one(chunk, o): load values qb .. qb+PARK_CH-1 of polynomial c
 //   store(qb, o0, o1): the same values of both polynomials;  flush(): stores are visible to later loads
-//   store_digits / load_digits: the 16 packed level-1 digit words that wait for the second
-//   forward transform of an accumulator polynomial
 #ifndef TFB_PARK_CH
 #define TFB_PARK_CH 4
 #endif
 constexpr int PARK_CH = TFB_PARK_CH;
+static_assert(PARK_CH == WCHUNK_Q, "one key chunk pairs with one accumulator chunk");
 struct RegPark {  // no parking: plain registers (host emulation)
   typedef MemChunk4 Chunk;
   cd v[2][WPTS];
@@ -442,29 +466,38 @@ struct RegPark {  // no parking: plain registers (host emulation)
     }
   }
   TFB_HD void flush() const {}
-  uint32_t d[WPTS];
-  TFB_HD void store_digits(const uint32_t* v) {
-#pragma unroll
-    for (int m = 0; m < WPTS; ++m) d[m] = v[m];
-  }
-  TFB_HD void load_digits(uint32_t* v) const {
-#pragma unroll
-    for (int m = 0; m < WPTS; ++m) v[m] = d[m];
-  }
 };
 
-// MAC of one forward-transformed digit polynomial x against level `lvl` of the staged key;
-// the accumulators live in the park.  FIRST starts them instead of loading them.
-template <bool FIRST, class BkSource, class Park>
-TFB_HD void wmac(Park& park, const cd* x, BkSource& bk, const cd* chunk, int t) {
-  const cd* key = chunk + t;
+// Spectral rotation factors of a pair for one lane: X^a at the point of register q is
+// base * exp(i pi a q / 8), base = exp(i pi a (1 + 4 r + 64 h) / N)  (wspectral_index: f = r + 16 h + 32 q).
+struct PairFactors {
+  cd base1, base2;
+  int a1, a2;
+};
+TFB_HD PairFactors pair_factors(const FactorTables* ft, int a1, int a2, int t) {
+  const uint32_t cl = 1u + 4u * (uint32_t)(t & 15) + 64u * (uint32_t)(t >> 4);
+  return PairFactors{unit_root(ft, (uint32_t)a1 * cl), unit_root(ft, (uint32_t)a2 * cl), a1, a2};
+}
+
+// MAC of one forward-transformed digit polynomial x (stage s of pair m) against the pair's three keys
+// combined with the rotation factors; the accumulators live in the park.  FIRST starts them instead of
+// loading them.  The warp takes its MAC turn once the first key chunk is resident.
+template <bool FIRST, class W, class BkSource, class Park>
+TFB_HD void wmac(Park& park, const cd* x, BkSource& bk, int m, int s, const PairFactors& pf, const FactorTables* ft,
+                 int t, W& w) {
   typename Park::Chunk ch0[2], ch1[2];
-  if (!FIRST) {
-    park.issue_one(0, 0, ch0[0]);
-    park.issue_one(1, 0, ch1[0]);
-  }
 #pragma unroll
   for (int qb = 0; qb < WPTS; qb += PARK_CH) {
+    const cd* key = bk.acquire_chunk(m, s, qb / PARK_CH) + t;
+    if (qb == 0) {
+      TFB_TICK(w, 4);
+      w.turn_enter();
+      TFB_TICK(w, 5);
+      if (!FIRST) {
+        park.issue_one(0, 0, ch0[0]);
+        park.issue_one(1, 0, ch1[0]);
+      }
+    }
     cd o0[PARK_CH], o1[PARK_CH];
     if (!FIRST) {
       const int cur = (qb / PARK_CH) & 1;
@@ -478,21 +511,29 @@ TFB_HD void wmac(Park& park, const cd* x, BkSource& bk, const cd* chunk, int t) 
 #pragma unroll
     for (int j = 0; j < PARK_CH; ++j) {
       const int q = qb + j;
-      const cd b0 = bk.load(key + wstage_index(0, q, 0, 0)), b1 = bk.load(key + wstage_index(0, q, 1, 0));
+      cd u1 = cmul(pf.base1, ft->A[(4 * pf.a1 * q) & 63]), u2 = cmul(pf.base2, ft->A[(4 * pf.a2 * q) & 63]);
+      u1.re -= 1.0;
+      u2.re -= 1.0;
+      const cd k0 = combine_keys(u1, u2, bk.load(key + wchunk_index(j, 0, 0, 0)), bk.load(key + wchunk_index(j, 1, 0, 0)),
+                                 bk.load(key + wchunk_index(j, 2, 0, 0)));
+      const cd k1 = combine_keys(u1, u2, bk.load(key + wchunk_index(j, 0, 1, 0)), bk.load(key + wchunk_index(j, 1, 1, 0)),
+                                 bk.load(key + wchunk_index(j, 2, 1, 0)));
       if (FIRST) {
-        o0[j] = cmul(x[q], b0);
-        o1[j] = cmul(x[q], b1);
+        o0[j] = cmul(x[q], k0);
+        o1[j] = cmul(x[q], k1);
       } else {
-        cmac(o0[j], x[q], b0);
-        cmac(o1[j], x[q], b1);
+        cmac(o0[j], x[q], k0);
+        cmac(o1[j], x[q], k1);
       }
     }
     park.store(qb, o0, o1);
+    if (qb + PARK_CH == WPTS) w.turn_leave();
+    bk.release();
   }
   park.flush();
 }
 
-// 10-bit digit field -> exact double of the signed digit (mantissa trick; an I2F.F64 measured 2 % slower)
+// unsigned digit field -> exact double of the signed digit (mantissa trick; an I2F.F64 measured 2 % slower)
 TFB_HD double wdigit(uint32_t field) { return digit_to_double(field); }
 // sg * digit for sg = +-1 (the lane sign of the odd inputs): one FMA instead of the DADD, exact
 TFB_HD double wdigit_signed(uint32_t field, double sg, double neg_sg_bias) {
@@ -503,68 +544,44 @@ TFB_HD uint32_t round_to_word_signed(double x, double sg) {
   return (uint32_t)double_to_bits(fma(x, sg, 6755399441055744.0));
 }
 
-// Stage s = 2p + lvl of a CMux: digits of accumulator polynomial p at gadget level lvl (read
-// and decomposed from ACC for lvl 0, which also parks the level-1 digit words; taken from the
-// park for lvl 1), forward transform, MAC against the key.
+// Stage s = 2p + lvl of a pair step: digits of accumulator polynomial p at gadget level lvl (both levels are
+// cut from the lane's own 32 words of ACC[p], eight 16-byte loads), forward transform, MAC against the keys.
 template <bool FIRST, class W, class BkSource, class Park, class Tw>
-TFB_HD void wcmux_stage(int s, const uint32_t* acc, int abar, int i, BkSource& bk, int t, const Tw& tw, void* buf,
-                        W& w, Park& park) {
+TFB_HD void wcmux_stage(int s, const uint32_t* acc, int m, const PairFactors& pf, const FactorTables* ft, BkSource& bk,
+                        int t, const Tw& tw, void* buf, W& w, Park& park) {
   const int p = s >> 1, lvl = s & 1;
   cd x[WPTS];
-  uint32_t d1[WPTS];  // level-1 digit fields of (re, im), 16 bits each
-  // lanes with h = 1 feed the transform -x[m] for odd m (see wfft_forward): sign folded into the conversion
-  const double sg = (t >> 4) ? -1.0 : 1.0, nsb = -sg * (4503599627370496.0 + 512.0);
-  if (lvl == 0) {
-    // The rotation indices depend only on (abar, lane); hidden behind an opaque copy the
-    // compiler recomputes them here instead of carrying 64 of them across the whole CMux.
-    int rot = abar;
-    TFB_OPAQUE(rot);
-    // coefficient j = t + 32 mm of X^rot * P - P, mm = 0..31 (mm >= 16: the imaginary parts):
-    // the source index advances by 32 per step in the doubled index space [0, 2N), whose
-    // bit 10 is the sign of the wrapped coefficient
-    const uint32_t* poly = acc + p * RING_N;
-    const uint32_t base = (uint32_t)(t - rot);
+  // lanes with h = 1 feed the transform -x[mm] for odd mm (see wfft_forward): sign folded into the conversion
+  const double sg = (t >> 4) ? -1.0 : 1.0, nsb = -sg * (4503599627370496.0 + (double)DIGIT_HALF);
+  const int shift = 32 - (lvl + 1) * BK_BGBIT;
+  const uint32_t* poly = acc + p * RING_N;
 #pragma unroll
-    for (int m = 0; m < WPTS; ++m) {
-      uint32_t v[2];
+  for (int u = 0; u < 4; ++u) {
+    const Words4 re = *reinterpret_cast<const Words4*>(poly + wacc_unit(t, u));
+    const Words4 im = *reinterpret_cast<const Words4*>(poly + wacc_unit(t, u + 4));
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const uint32_t src = base + 32u * (uint32_t)(m + 16 * e);
-        const uint32_t sg = (uint32_t)((int32_t)(src << 21) >> 31);  // all ones when the wrap flips the sign
-        v[e] = ((poly[src & (RING_N - 1)] ^ sg) - sg) - poly[t + 32 * (m + 16 * e)] + DECOMP_OFFSET;
-      }
-      x[m] = (m & 1) ? cd{wdigit_signed(v[0] >> 22, sg, nsb), wdigit_signed(v[1] >> 22, sg, nsb)}
-                     : cd{wdigit(v[0] >> 22), wdigit(v[1] >> 22)};
-      d1[m] = ((v[0] >> 12) & 0x3ffu) | ((v[1] << 4) & 0x3ff0000u);
+    for (int e = 0; e < 4; ++e) {
+      const int mm = 4 * u + e;
+      const uint32_t fr = ((re.w[e] + DECOMP_OFFSET) >> shift) & ((1u << BK_BGBIT) - 1);
+      const uint32_t fi = ((im.w[e] + DECOMP_OFFSET) >> shift) & ((1u << BK_BGBIT) - 1);
+      x[mm] = (mm & 1) ? cd{wdigit_signed(fr, sg, nsb), wdigit_signed(fi, sg, nsb)} : cd{wdigit(fr), wdigit(fi)};
     }
-    park.store_digits(d1);
-  } else {
-    park.load_digits(d1);
-#pragma unroll
-    for (int m = 0; m < WPTS; ++m)
-      x[m] = (m & 1) ? cd{wdigit_signed(d1[m] & 0xffffu, sg, nsb), wdigit_signed(d1[m] >> 16, sg, nsb)}
-                     : cd{wdigit(d1[m] & 0xffffu), wdigit(d1[m] >> 16)};
   }
   wfft_forward<false>(x, t, tw, buf, w);
-  const cd* chunk = bk.acquire_chunk(i, p, lvl);
-  TFB_TICK(w, 4);
-  w.turn_enter();
-  TFB_TICK(w, 5);
-  wmac<FIRST>(park, x, bk, chunk, t);
-  w.turn_leave();
-  bk.release();
+  wmac<FIRST>(park, x, bk, m, s, pf, ft, t, w);
   TFB_TICK(w, 6);
 }
 
-// One CMux step by one warp.  acc: 2 polynomials of N words in shared memory.
+// One pair step by one warp.  acc: 2 polynomials of N words in shared memory (WarpAccLayout).
 // Stage 0 starts the accumulators; stages 1..3 and the two inverse transforms run as rolled
 // loops (TFB_K1D_ROLL): one copy of the transform code in the instruction cache.
 template <class W, class BkSource, class Park, class Tw>
-TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, const Tw& tw, void* buf, W& w,
-                       Park& park) {
-  wcmux_stage<true>(0, acc, abar, i, bk, t, tw, buf, w, park);
+TFB_HD void wcmux_step(uint32_t* acc, int m, int a1, int a2, const FactorTables* ft, BkSource& bk, int t, const Tw& tw,
+                       void* buf, W& w, Park& park) {
+  const PairFactors pf = pair_factors(ft, a1, a2, t);
+  wcmux_stage<true>(0, acc, m, pf, ft, bk, t, tw, buf, w, park);
   TFB_K1D_LOOP
-  for (int s = 1; s < 4; ++s) wcmux_stage<false>(s, acc, abar, i, bk, t, tw, buf, w, park);
+  for (int s = 1; s < 4; ++s) wcmux_stage<false>(s, acc, m, pf, ft, bk, t, tw, buf, w, park);
   TFB_K1D_LOOP
   for (int c = 0; c < 2; ++c) {
     cd x[WPTS];
@@ -576,11 +593,21 @@ TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, cons
       for (int qb = 0; qb < WPTS; qb += PARK_CH) park.settle_one(ch[qb / PARK_CH], x + qb);
     }
     wfft_inverse<false>(x, t, tw, buf, w);
-    const double sg = (t >> 4) ? -1.0 : 1.0;  // the inverse leaves -x[m] for odd m on the lanes with h = 1
+    const double sg = (t >> 4) ? -1.0 : 1.0;  // the inverse leaves -x[mm] for odd mm on the lanes with h = 1
+    uint32_t* poly = acc + c * RING_N;
 #pragma unroll
-    for (int m = 0; m < WPTS; ++m) {
-      acc[c * RING_N + t + 32 * m] += (m & 1) ? round_to_word_signed(x[m].re, sg) : round_to_word(x[m].re);
-      acc[c * RING_N + t + 32 * m + HALF_N] += (m & 1) ? round_to_word_signed(x[m].im, sg) : round_to_word(x[m].im);
+    for (int u = 0; u < 4; ++u) {
+      Words4* pr = reinterpret_cast<Words4*>(poly + wacc_unit(t, u));
+      Words4* pi = reinterpret_cast<Words4*>(poly + wacc_unit(t, u + 4));
+      Words4 re = *pr, im = *pi;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int mm = 4 * u + e;
+        re.w[e] += (mm & 1) ? round_to_word_signed(x[mm].re, sg) : round_to_word(x[mm].re);
+        im.w[e] += (mm & 1) ? round_to_word_signed(x[mm].im, sg) : round_to_word(x[mm].im);
+      }
+      *pr = re;
+      *pi = im;
     }
     TFB_TICK(w, 11);
   }
@@ -588,29 +615,35 @@ TFB_HD void wcmux_step(uint32_t* acc, int abar, int i, BkSource& bk, int t, cons
 }
 
 // Whole gate bootstrap (without key switch) for one ciphertext by one warp.
-//   sm_acc: 2N words, sm_abar: n+1 uint16, buf: WBUF_BYTES, ext: N+1 words out
+//   sm_acc: 2N words, sm_abar: n+2 uint16, buf: WBUF_BYTES, ext: N+1 words out
 template <class W, class BkSource, class Park, class Tw>
 TFB_HD void gate_bootstrap_warp(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu,
-                                BkSource& bk, const Tw& tw, uint32_t* sm_acc, uint16_t* sm_abar,
+                                BkSource& bk, const Tw& tw, const FactorTables* ft, uint32_t* sm_acc, uint16_t* sm_abar,
                                 void* buf, uint32_t* ext, int t, W& w, Park& park) {
-  bootstrap_prologue(x_row, y_row, kind, n, mu, sm_acc, sm_abar, t, WARP_T, w);
+  bootstrap_prologue(x_row, y_row, kind, n, mu, sm_acc, sm_abar, t, WARP_T, w, WarpAccLayout());
+  const int pairs = (n + 1) / 2;
 #pragma unroll 1
-  for (int i = 0; i < n; ++i) {
-    const int abar = sm_abar[i];
-    if (abar == 0) {  // uniform across the warp: X^0 - 1 = 0, the CMux is the identity
-      // keep the key ring and the turn protocol in step, in the order a real CMux takes them (a warp that
-      // held its turns back while it drained four chunks would stall the ring its partners wait on)
+  for (int m = 0; m < pairs; ++m) {
+    int a1, a2;
+    pair_rotations(sm_abar, n, m, a1, a2);
+    if ((a1 | a2) == 0) {  // uniform across the warp: both factors vanish, the step is the identity
+      // keep the key ring and the turn protocol in step, in the order a real step takes them (a warp that
+      // held its turns back while it drained a pair's chunks would stall the ring its partners wait on)
 #pragma unroll 1
       for (int s = 0; s < 4; ++s) {
-        bk.acquire_chunk(i, s >> 1, s & 1);
-        w.turn_pass();
-        bk.release();
+#pragma unroll 1
+        for (int qc = 0; qc < WPTS / WCHUNK_Q; ++qc) {
+          bk.acquire_chunk(m, s, qc);
+          if (qc == 0) w.turn_enter();
+          if (qc + 1 == WPTS / WCHUNK_Q) w.turn_leave();
+          bk.release();
+        }
       }
       continue;
     }
-    wcmux_step(sm_acc, abar, i, bk, t, tw, buf, w, park);
+    wcmux_step(sm_acc, m, a1, a2, ft, bk, t, tw, buf, w, park);
   }
-  if (ext) bootstrap_extract(sm_acc, ext, t, WARP_T);  // null: surplus warp of a tail CTA
+  if (ext) bootstrap_extract(sm_acc, ext, t, WARP_T, WarpAccLayout());  // null: surplus warp of a tail CTA
 }
 
 }  // namespace tfb

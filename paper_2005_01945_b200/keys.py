@@ -5,8 +5,14 @@ alpha = 2**-15, 32-bit torus, mu = 1/8: `encirc/torus.py:25-27,118-134`) and
 replaces the bootstrap with a key-holding oracle (`encirc/engine.py:493-503`).
 A real gate bootstrap needs the ring half as well.  We take the TFHE
 "110-bit" gate-bootstrapping set the paper says its framework is analogous
-to: N = 1024, k = 1, gadget l = 2 / Bg = 2**10, key switch
-t = 8 digits of base 2**2, sigma_bk = 7.18e-9, sigma_ks = alpha.
+to: N = 1024, k = 1, key switch t = 8 digits of base 2**2,
+sigma_bk = 7.18e-9, sigma_ks = alpha -- with two changes that belong together:
+the bootstrapping key is UNROLLED over pairs of LWE mask elements (Zhou et al.
+2018, Bourse et al. 2018: three TRGSW samples s1, s2, s1*s2 per pair, half as
+many CMux steps) and the gadget is l = 2 / Bg = 2**9 instead of 2**10, which
+pays for the unrolling's larger key-noise term (3 external products per pair,
+factors |X**a - 1|**2 ~ 2 and 4) so that the output noise stays where the
+plain set had it.
 
 Everything here runs once per engine on the host with numpy; the results are
 raw torus words.  The device turns the bootstrapping key into its spectral
@@ -15,9 +21,13 @@ layout itself (`tfb_load_keys`, kernel K3 in `csrc/tfhe_b200.cu`).
 Layouts (all int32 bit patterns of uint32 torus words):
 
   ring key   s'[N]                    bits 0/1
-  bk         [n][(k+1)*l][k+1][N]     row r = p*l + lvl is a TRLWE sample
-                                      (a, b) of 0 under s' whose component p
-                                      carries s_i * 2**(32 - (lvl+1)*bgbit)
+  bk         [ceil(n/2)][3][(k+1)*l][k+1][N]
+                                      pair m, key j: TRGSW of s_2m (j = 0),
+                                      s_2m+1 (j = 1), s_2m * s_2m+1 (j = 2; an
+                                      odd n pads s_n = 0); row r = p*l + lvl is
+                                      a TRLWE sample (a, b) of 0 under s' whose
+                                      component p carries
+                                      message * 2**(32 - (lvl+1)*bgbit)
   ksk        [N][t][n+1]              LWE_s( s'_i * 2**(32 - (j+1)*basebit) ),
                                       mask words then body
 
@@ -38,6 +48,7 @@ from .torus import SecretKey
 RING_KEY_STREAM = 3
 BK_STREAM = 4
 KSK_STREAM = 5
+BK_KEYS = 3  # TRGSW samples per pair of mask elements: s1, s2, s1 * s2
 
 
 @dataclass(frozen=True)
@@ -47,7 +58,7 @@ class RingParams:
     N: int = 1024
     k: int = 1
     bk_l: int = 2
-    bk_bgbit: int = 10
+    bk_bgbit: int = 9
     ks_t: int = 8
     ks_basebit: int = 2
     bk_stdev: float = 7.18e-9
@@ -77,7 +88,7 @@ class EvaluationKeys:
     ring: RingParams
     n: int
     ring_key: np.ndarray  # int32[N]
-    bk: np.ndarray  # int32[n][rows][2][N]
+    bk: np.ndarray  # int32[ceil(n/2)][3][rows][2][N]
     ksk: np.ndarray  # int32[N][t][n+1]
 
 
@@ -117,16 +128,20 @@ def generate_evaluation_keys(key: SecretKey, seed: int, ring: RingParams | None 
 
     ring_key = np.random.default_rng((seed, RING_KEY_STREAM)).integers(0, 2, size=N).astype(np.uint32)
 
-    # bootstrapping key: n TRGSW samples = n * rows TRLWE rows
+    # bootstrapping key, unrolled over pairs of mask elements: 3 TRGSW samples per pair
+    pairs = (n + 1) // 2
+    s_pad = np.concatenate([s, np.zeros(2 * pairs - n, dtype=np.uint32)])
+    s1, s2 = s_pad[0::2], s_pad[1::2]
+    messages = np.stack([s1, s2, s1 * s2], axis=1)  # [pairs][3]
     rng = np.random.default_rng((seed, BK_STREAM))
-    mask = rng.integers(0, 1 << 32, size=(n, rows, N), dtype=np.uint32)
-    noise = _gauss_words(rng, ring.bk_stdev, (n, rows, N))
+    mask = rng.integers(0, 1 << 32, size=(pairs, BK_KEYS, rows, N), dtype=np.uint32)
+    noise = _gauss_words(rng, ring.bk_stdev, (pairs, BK_KEYS, rows, N))
     body = negacyclic_mul_binary(mask, ring_key) + noise
-    bk = np.stack([mask, body], axis=2)  # [n][rows][2][N]
+    bk = np.stack([mask, body], axis=3)  # [pairs][3][rows][2][N]
     for p_idx in range(ring.k + 1):
         for lvl in range(ring.bk_l):
             gadget = np.uint32(1 << (32 - (lvl + 1) * ring.bk_bgbit))
-            bk[:, p_idx * ring.bk_l + lvl, p_idx, 0] += s * gadget
+            bk[:, :, p_idx * ring.bk_l + lvl, p_idx, 0] += messages * gadget
 
     # key-switching key: N * t LWE samples under s
     rng = np.random.default_rng((seed, KSK_STREAM))

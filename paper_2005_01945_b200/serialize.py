@@ -12,7 +12,7 @@ length-prefixed sequences:
     vector  'V'  u32 length | length int bodies
     matrix  'M'  u32 rows | u32 cols | rows*cols int bodies, row-major
     evalkey 'E'  (extension) u32 n | u32 N | u8 l | u8 bgbit | u8 t | u8 basebit |
-                 N ring-key bytes | bk int32[n][2l][2][N] | ksk int32[N][t][n+1]
+                 N ring-key bytes | bk int32[ceil(n/2)][3][2l][2][N] | ksk int32[N][t][n+1]
 
 Ciphertexts of a device engine are moved in bulk: all sample bodies of an
 integer / vector / matrix are one structured numpy array filled from one
@@ -28,7 +28,7 @@ import struct
 import numpy as np
 
 from .integers import EncryptedInt
-from .keys import EvaluationKeys, RingParams
+from .keys import BK_KEYS, EvaluationKeys, RingParams
 from .linalg import EncryptedIntVector, EncryptedMatrix
 from .torus import LweParams, LweSample, SecretKey, TorusElement, word_dtype
 
@@ -284,7 +284,8 @@ def load_eval_keys(data: bytes) -> EvaluationKeys:
     ring_key = np.frombuffer(c.take(N), dtype=np.uint8)
     if ring_key.max(initial=0) > 1:
         raise FormatError("ring key bits must be 0 or 1")
-    bk = np.frombuffer(c.take(4 * n * ring.rows * 2 * N), dtype="<i4").reshape(n, ring.rows, 2, N)
+    pairs = (n + 1) // 2  # the bootstrapping key is unrolled over pairs of mask elements: keys s1, s2, s1*s2
+    bk = np.frombuffer(c.take(4 * pairs * BK_KEYS * ring.rows * 2 * N), dtype="<i4").reshape(pairs, BK_KEYS, ring.rows, 2, N)
     ksk = np.frombuffer(c.take(4 * N * t * (n + 1)), dtype="<i4").reshape(N, t, n + 1)
     c.finish()
     return EvaluationKeys(ring=ring, n=n, ring_key=ring_key.astype(np.int32), bk=bk.copy(), ksk=ksk.copy())

@@ -174,17 +174,17 @@ def gather_lanes(engine, local, lanes: int, root: int = 0, group=None):
 
 
 def broadcast_eval_keys(key, seed: int, device, ring=None, root: int = 0, group=None) -> tuple:
-    """Evaluation keys generated on the root only and broadcast RAW (bk 16.4 MB, ksk 16.4 MB of int32 words) to
+    """Evaluation keys generated on the root only and broadcast RAW (bk 24.6 MB, ksk 16.4 MB of int32 words) to
     every rank's GPU; each GPU turns them into its spectral / tiled layouts itself (`tfb_load_keys`, kernel K3).
     Returns the device tensors (bk, ksk) to hand to `B200Engine(raw_key_tensors=...)`."""
     import torch
 
-    from .keys import RingParams, generate_evaluation_keys
+    from .keys import BK_KEYS, RingParams, generate_evaluation_keys
 
     ring = ring if ring is not None else RingParams()
     world, rank = _world(group)
     n = key.params.m
-    bk = torch.empty((n, ring.rows, 2, ring.N), dtype=torch.int32, device=device)
+    bk = torch.empty(((n + 1) // 2, BK_KEYS, ring.rows, 2, ring.N), dtype=torch.int32, device=device)
     ksk = torch.empty((ring.N, ring.ks_t, n + 1), dtype=torch.int32, device=device)
     if rank == root:
         ek = generate_evaluation_keys(key, seed, ring)

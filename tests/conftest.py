@@ -59,7 +59,7 @@ def emu_lib():
     import ctypes
 
     src = os.path.join(ROOT, "tests", "emu", "emu_bootstrap.cpp")
-    hdrs = [os.path.join(ROOT, "paper_2005_01945_b200", "csrc", h) for h in ("tfhe_device.cuh", "tfhe_warp.cuh")]
+    hdrs = [os.path.join(ROOT, "paper_2005_01945_b200", "csrc", h) for h in ("tfhe_device.cuh", "tfhe_warp.cuh", "tfhe_pair.cuh")]
     so = os.path.join(ROOT, "tests", "emu", "libtfhe_emu.so")
     if not os.path.exists(so) or os.path.getmtime(so) < max(os.path.getmtime(f) for f in [src, *hdrs]):
         subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", "-o", so, src])

@@ -58,16 +58,15 @@ def test_k1_dispatch_plan(library):
     warp-per-gate kernel for wide ones, full K1d waves + a cheaper tail for ragged wide launches."""
     pick = _cabi.pick_kernel
     assert pick(1) == (5, 0) and pick(2) == (5, 0) and pick(74) == (5, 0)    # adders / multiplier trees: one gate per 2-SM cluster
-    assert pick(75) == (3, 0) and pick(148) == (3, 0)                         # up to one gate per SM: K1c
-    assert pick(592)[0] == 2 and pick(1184)[0] == 2                           # one / two waves of 4-gate CTAs
+    assert pick(148) == (5, 0) and pick(592)[0] == 5                          # a few cluster waves still beat one warp-kernel wave
     assert pick(1776) == (4, 0) and pick(3552) == (4, 0)                      # full waves of 12-gate CTAs
     which, body = pick(1 << 16)                                               # BASELINE configs[1]
     assert body in (0, 36 * 1776) and (body or which == 4)
-    which, body = pick(2 * 1776 + 300)                                        # ragged: K1d waves, then a short tail
-    assert body == 2 * 1776 and which in (1, 2, 3)
+    which, body = pick(2 * 1776 + 30)                                         # ragged: K1d waves, then a short tail on the clusters
+    assert body == 2 * 1776 and which == 5
     for k in (1, 7, 149, 297, 600, 1000, 1777, 5000, 100000):
         which, body = pick(k)
-        assert which in (1, 2, 3, 4, 5) and 0 <= body < k and body % 1776 == 0
+        assert which in (4, 5) and 0 <= body < k and body % 1776 == 0
     assert pick(1776 // 2, sms=74) == (4, 0)                                  # scales with the SM count
 
 

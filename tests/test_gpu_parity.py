@@ -63,10 +63,10 @@ def test_spectral_key_matches_numpy(gpu, eval_keys):
     ctx, torch, _cabi = gpu
     N = 1024
     tw = np.exp(1j * np.pi * np.arange(N // 2) / N)
-    for i in (0, 3, 499):
+    for m, j in ((0, 0), (3, 1), (249, 2)):  # (pair of mask elements, key s1 / s2 / s1*s2)
         spec = np.empty((4, 2, 512, 2), dtype=np.float64)
-        ctx.call("tfb_debug_spectral_key", i, spec.ctypes.data)
-        poly = eval_keys.bk[i].astype(np.float64)
+        ctx.call("tfb_debug_spectral_key", m, j, spec.ctypes.data)
+        poly = eval_keys.bk[m, j].astype(np.float64)
         want = np.fft.ifft((poly[..., : N // 2] + 1j * poly[..., N // 2 :]) * tw, axis=-1) * (N // 2)
         got = spec[..., 0] + 1j * spec[..., 1]
         assert np.abs(got - want).max() / np.abs(want).max() < 1e-13
@@ -121,9 +121,8 @@ def test_edge_inputs_trivial_and_aliased(gpu, key, eval_keys):
 
 
 def test_every_kernel_variant_is_bit_exact(key, eval_keys, monkeypatch):
-    """K1a (one gate per 64-thread CTA), K1b (four gates per CTA, TMA-staged key ring), K1c (one gate
-    over four thread groups), K1d (one gate per warp, twelve per CTA, tensor-memory parking), K1e (one gate per
-    two-CTA cluster, contributions exchanged through distributed shared memory) and the
+    """K1d (one gate per warp, twelve per CTA, TMA-staged key ring, tensor-memory parking), K1e (one gate per
+    two-CTA cluster, key combiner warps, contributions exchanged through distributed shared memory) and the
     key-switch kernels (K2 direct / split with atomics on the IMAD pipe, K2t on the tensor cores) on the
     same jobs, with a gate count that leaves a ragged last CTA / a partial 128-gate tile."""
     import torch
@@ -132,7 +131,7 @@ def test_every_kernel_variant_is_bit_exact(key, eval_keys, monkeypatch):
 
     xs, ys, kinds, bits = make_inputs(key, 45, seed=36, kinds=(np.arange(45) % 9).astype(np.uint8))
     want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
-    for variant, ks in (("1", "1"), ("2", "2"), ("3", "1"), ("4", "2"), ("4", "1"), ("5", "1"), ("5", "2")):
+    for variant, ks in (("4", "2"), ("4", "1"), ("5", "1"), ("5", "2")):
         monkeypatch.setenv("TFB_FORCE_KERNEL", variant)
         monkeypatch.setenv("TFB_FORCE_KS", ks)  # 1 = K2 (IMAD pipe), 2 = K2t (tcgen05.mma kind::i8)
         ctx = _cabi.Context(0, key.params.m, key.params.mu.word, eval_keys.ring)
@@ -184,9 +183,9 @@ def test_key_switch_on_tensor_cores_is_exact(key, eval_keys, monkeypatch):
         ctx.close()
 
 
-@pytest.mark.parametrize("n", [7, 511])
+@pytest.mark.parametrize("n", [7, 510])
 def test_other_lwe_dimensions_through_the_host_path(n, monkeypatch):
-    """The smallest and the largest LWE dimension the library accepts (rows of n + 1 <= 512 words), every
+    """A small odd and the largest LWE dimension the library accepts (rows of n + 2 <= 512 words), every
     K1 / K2 variant and the automatic split dispatch, through tfb_gate_launch_host (packed rows)."""
     from paper_2005_01945_b200 import LweParams, _cabi, generate_evaluation_keys, keygen
 
@@ -196,7 +195,7 @@ def test_other_lwe_dimensions_through_the_host_path(n, monkeypatch):
     K = 8
     xs, ys, kinds, _ = make_inputs(k, K, seed=8, kinds=(np.arange(K) % 8).astype(np.uint8))
     want = orc.gate_bootstrap_batch(xs, ys, kinds, p.mu.word, ek.bk, ek.ksk, fft=True)
-    for which, ks, count in (("3", "1", 8), ("1", "1", 8), ("2", "2", 200), ("4", "2", 200), ("4", "1", 13), (None, None, 3000)):
+    for which, ks, count in (("5", "1", 8), ("5", "2", 200), ("4", "2", 200), ("4", "1", 13), (None, None, 3000)):
         for name, val in (("TFB_FORCE_KERNEL", which), ("TFB_FORCE_KS", ks)):
             monkeypatch.setenv(name, val) if val else monkeypatch.delenv(name, raising=False)
         ctx = _cabi.Context(0, n, p.mu.word, ek.ring)
@@ -210,7 +209,7 @@ def test_other_lwe_dimensions_through_the_host_path(n, monkeypatch):
 
 
 def test_automatic_dispatch_sizes(gpu, key, eval_keys):
-    """Launch sizes on both sides of the K1c / K1a / K1b / K1d dispatch thresholds (2, 4, 12 x SMs)."""
+    """Launch sizes on both sides of the K1e / K1d dispatch threshold and of a full K1d wave (12 x SMs)."""
     base = 64
     xs, ys, kinds, bits = make_inputs(key, base, seed=37)
     want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)

@@ -40,7 +40,7 @@ def test_keys_are_deterministic_and_shaped(key, eval_keys):
     assert np.array_equal(again.bk, eval_keys.bk) and np.array_equal(again.ksk, eval_keys.ksk)
     other = generate_evaluation_keys(key, seed=12)
     assert not np.array_equal(other.ring_key, eval_keys.ring_key)
-    assert eval_keys.bk.shape == (500, 4, 2, 1024) and eval_keys.ksk.shape == (1024, 8, 501)
+    assert eval_keys.bk.shape == (250, 3, 4, 2, 1024) and eval_keys.ksk.shape == (1024, 8, 501)
     assert set(np.unique(eval_keys.ring_key)) <= {0, 1}
     with pytest.raises(ValueError):
         RingParams(k=2)
@@ -48,27 +48,47 @@ def test_keys_are_deterministic_and_shaped(key, eval_keys):
         RingParams(N=1000)
 
 
-def test_bootstrapping_key_rows_decrypt_to_gadget_times_key_bit(key, eval_keys):
-    """TRLWE row (p, lvl) of BK_i has phase  s_i * 2^(32-(lvl+1)*10) * [X^0 of component p]  + small noise."""
+def test_bootstrapping_key_rows_decrypt_to_gadget_times_message(key, eval_keys):
+    """TRLWE row (p, lvl) of key j of pair m has phase  msg * 2^(32-(lvl+1)*bgbit) * [X^0 of component p]  + small
+    noise, msg = s_2m, s_2m+1, s_2m * s_2m+1 for j = 0, 1, 2 (the unrolled bootstrapping key)."""
     ring = eval_keys.ring
     sprime = eval_keys.ring_key.view(np.uint32)
-    for i in (0, 1, 7, 499):
-        s_i = int(key.bits[i])
-        for r in range(4):
-            p_idx, lvl = divmod(r, ring.bk_l)
-            a = eval_keys.bk[i, r, 0].view(np.uint32)
-            b = eval_keys.bk[i, r, 1].view(np.uint32)
-            ph = orc.ring_phase(a, b, sprime).astype(np.int64)
-            gadget = s_i << (32 - (lvl + 1) * ring.bk_bgbit)
-            # message polynomial: component 1 (b) carries +gadget at X^0; component 0 (a) carries
-            # gadget * (-s') after taking the phase b - a*s'
-            want = np.zeros(1024, dtype=np.int64)
-            if p_idx == 1:
-                want[0] = gadget
-            else:
-                want = -(gadget * sprime.astype(np.int64))
-            err = ((ph - want + 2**31) % 2**32) - 2**31
-            assert np.abs(err).max() < 400  # 7.18e-9 * 2^32 = 31 -> 400 is ~13 sigma
+    for m in (0, 3, 249):
+        s1, s2 = int(key.bits[2 * m]), int(key.bits[2 * m + 1])
+        for j, msg in enumerate((s1, s2, s1 * s2)):
+            for r in range(4):
+                p_idx, lvl = divmod(r, ring.bk_l)
+                a = eval_keys.bk[m, j, r, 0].view(np.uint32)
+                b = eval_keys.bk[m, j, r, 1].view(np.uint32)
+                ph = orc.ring_phase(a, b, sprime).astype(np.int64)
+                gadget = msg << (32 - (lvl + 1) * ring.bk_bgbit)
+                # message polynomial: component 1 (b) carries +gadget at X^0; component 0 (a) carries
+                # gadget * (-s') after taking the phase b - a*s'
+                want = np.zeros(1024, dtype=np.int64)
+                if p_idx == 1:
+                    want[0] = gadget
+                else:
+                    want = -(gadget * sprime.astype(np.int64))
+                err = ((ph - want + 2**31) % 2**32) - 2**31
+                assert np.abs(err).max() < 400  # 7.18e-9 * 2^32 = 31 -> 400 is ~13 sigma
+
+
+def test_odd_dimension_pads_the_last_pair_with_a_zero_key_bit():
+    p = LweParams(m=7)
+    k = keygen(p, seed=3)
+    ek = generate_evaluation_keys(k, seed=3)
+    assert ek.bk.shape == (4, 3, 4, 2, 1024)
+    sprime = ek.ring_key.view(np.uint32)
+    for j, msg in enumerate((int(k.bits[6]), 0, 0)):  # s_7 = 0: keys 1 and 2 of the last pair encrypt 0
+        ph = orc.ring_phase(ek.bk[3, j, 2, 0].view(np.uint32), ek.bk[3, j, 2, 1].view(np.uint32), sprime).astype(np.int64)
+        want = np.zeros(1024, dtype=np.int64)
+        want[0] = msg << (32 - ring_bgbit(ek))
+        err = ((ph - want + 2**31) % 2**32) - 2**31
+        assert np.abs(err).max() < 400
+
+
+def ring_bgbit(ek):
+    return ek.ring.bk_bgbit
 
 
 def test_key_switching_key_rows_decrypt(key, eval_keys):
@@ -147,12 +167,12 @@ def test_key_switch_digits_recompose():
     assert np.abs(err).max() <= 1 << 15
 
 
-def test_kernel_arithmetic_on_host_threads_matches_oracle(emu_lib, key):
-    """The exact __host__ __device__ code of kernel K1 (forward/inverse FFT,
-    CMux, rotation, decomposition, sample extract), driven by 64 host threads,
-    against the integer oracle.  Small LWE dimension keeps it to seconds; the
-    ring side is the production one."""
-    n = 12
+@pytest.mark.parametrize("n", [12, 7])
+def test_kernel_arithmetic_on_host_threads_matches_oracle(emu_lib, n):
+    """The exact __host__ __device__ code of the K1 kernels (forward/inverse FFT, spectral rotation factors, key
+    combination, decomposition, sample extract), driven by host threads, against the integer oracle: K1d (one
+    ciphertext per warp, 32 threads) and K1e (one ciphertext over two CTAs of two 64-thread groups, 256 threads).
+    Small LWE dimensions (even and odd: the padded last pair) keep it to seconds; the ring side is the production one."""
     p = LweParams(m=n)
     k = keygen(p, seed=3)
     ek = generate_evaluation_keys(k, seed=3)
@@ -162,25 +182,32 @@ def test_kernel_arithmetic_on_host_threads_matches_oracle(emu_lib, key):
     ys = np.stack([pack(encrypt_bit(k, (g >> 1) & 1, rng)) for g in range(K)])
     kinds = np.array([0, 4, 2, 7, 5, 8], dtype=np.uint8)
     out, ext = orc.gate_bootstrap_batch(xs, ys, kinds, p.mu.word, ek.bk, ek.ksk, want_ext=True)
-    bkf = np.empty((n, 4, 8, 2, 64, 2), dtype=np.float64)
+    pairs = (n + 1) // 2
     vp = ctypes.c_void_p
+    # K1e: chunks [pair][p][lvl][half][k4][key][c][t]
+    bkf = np.empty((pairs, 2, 2, 2, 4, 3, 2, 64, 2), dtype=np.float64)
     emu_lib.emu_bk_transform(vp(ek.bk.ctypes.data), n, vp(bkf.ctypes.data))
     got = np.empty((K, 1025), dtype=np.uint32)
-    emu_lib.emu_gate_bootstrap(vp(xs.ctypes.data), vp(ys.ctypes.data), vp(kinds.ctypes.data), ctypes.c_int64(K), n,
-                               ctypes.c_uint32(p.mu.word), vp(bkf.ctypes.data), vp(got.ctypes.data))
+    emu_lib.emu_pair_gate_bootstrap(vp(xs.ctypes.data), vp(ys.ctypes.data), vp(kinds.ctypes.data), ctypes.c_int64(K), n,
+                                    ctypes.c_uint32(p.mu.word), vp(bkf.ctypes.data), vp(got.ctypes.data))
     assert np.array_equal(got, ext)
-    # the latency variant (one ciphertext over four thread groups) must produce the same words
-    wide = np.empty((K, 1025), dtype=np.uint32)
-    emu_lib.emu_gate_bootstrap_wide(vp(xs.ctypes.data), vp(ys.ctypes.data), vp(kinds.ctypes.data), ctypes.c_int64(K),
-                                    n, ctypes.c_uint32(p.mu.word), vp(bkf.ctypes.data), vp(wide.ctypes.data))
-    assert np.array_equal(wide, ext)
-    # K1d (one ciphertext per warp, radix-16 transforms, its own spectral key order)
-    bkw = np.empty((n, 2, 2, 16, 2, 32, 2), dtype=np.float64)
+    # K1d: chunks [pair][stage][qc][q4][key][c][lane]
+    bkw = np.empty((pairs, 4, 4, 4, 3, 2, 32, 2), dtype=np.float64)
     emu_lib.emu_w_bk_transform(vp(ek.bk.ctypes.data), n, vp(bkw.ctypes.data))
     warp = np.empty((K, 1025), dtype=np.uint32)
     emu_lib.emu_w_gate_bootstrap(vp(xs.ctypes.data), vp(ys.ctypes.data), vp(kinds.ctypes.data), ctypes.c_int64(K), n,
                                  ctypes.c_uint32(p.mu.word), vp(bkw.ctypes.data), vp(warp.ctypes.data))
     assert np.array_equal(warp, ext)
+    # a gate on trivial inputs (every rotation zero) skips every step in both kernels
+    triv = np.zeros((2, n + 1), dtype=np.uint32)
+    triv[:, n] = [p.message_word(1), p.message_word(0)]
+    tk = np.array([2, 2], dtype=np.uint8)
+    _, text = orc.gate_bootstrap_batch(triv, triv[::-1].copy(), tk, p.mu.word, ek.bk, ek.ksk, want_ext=True)
+    for fn, key_arr in ((emu_lib.emu_pair_gate_bootstrap, bkf), (emu_lib.emu_w_gate_bootstrap, bkw)):
+        tg = np.empty((2, 1025), dtype=np.uint32)
+        fn(vp(triv.ctypes.data), vp(triv[::-1].copy().ctypes.data), vp(tk.ctypes.data), ctypes.c_int64(2), n,
+           ctypes.c_uint32(p.mu.word), vp(key_arr.ctypes.data), vp(tg.ctypes.data))
+        assert np.array_equal(tg, text)
     # K2's digit extraction against the oracle's key switch
     digits = np.empty((1024, 8), dtype=np.int32)
     emu_lib.emu_ks_digits(vp(ext[0].ctypes.data), vp(digits.ctypes.data))

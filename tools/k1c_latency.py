@@ -1,5 +1,5 @@
-"""Latency of one bootstrap (blind rotation only) on the latency kernels: K1c (one gate over four thread groups of one SM)
-and K1e (one gate per two-SM cluster), k gates per launch, checked word for word against the CPU oracle.
+"""Latency of one bootstrap (blind rotation only) on the latency kernel K1e (one gate per two-SM cluster) and, for
+comparison, one wave of the throughput kernel K1d, k gates per launch, checked word for word against the CPU oracle.
     python tools/k1c_latency.py [lib.so]"""
 import os, sys, numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -19,7 +19,7 @@ ys = np.stack([pack(encrypt_bit(key, g & 1, rng)) for g in range(K)])
 kinds = np.array([g % 8 for g in range(K)], dtype=np.uint8)
 _, want = orc.gate_bootstrap_batch(xs, ys, kinds, p.mu.word, ek.bk, ek.ksk, want_ext=True)
 dev = torch.device("cuda:0")
-for which, name in (("3", "K1c k_gate_bootstrap_wide"), ("5", "K1e k_gate_bootstrap_pair")):
+for which, name in (("5", "K1e k_gate_bootstrap_pair"), ("4", "K1d k_gate_bootstrap_warp")):
     os.environ["TFB_FORCE_KERNEL"] = which
     ctx = _cabi.Context(0, n, p.mu.word, ek.ring)
     ctx.call("tfb_load_keys", ek.bk.ctypes.data, ek.ksk.ctypes.data, 0, None)
