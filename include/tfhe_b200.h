@@ -124,12 +124,11 @@ int tfb_debug_key_switch(tfb_ctx *ctx, const uint32_t *ext_dev, void *pool_dev, 
  * natural frequency order and un-scaled: double[4][2][512][2] (row, component, frequency, re/im). */
 int tfb_debug_spectral_key(tfb_ctx *ctx, int32_t pair, int32_t key, double *out_host);
 
-/* K1 dispatch, host logic only (no GPU needed): which fused-bootstrap variant a launch of k gates
- * takes on a device with `sms` multiprocessors.  Returns 4 = K1d (one gate per warp, twelve per CTA:
- * throughput) or 5 = K1e (one gate per two-CTA cluster: latency).  When a large launch is split, *body_gates
- * receives the number of leading gates that run as full K1d waves and the return value is the
- * variant of the remaining k - *body_gates gates; otherwise *body_gates = 0. */
-int tfb_debug_pick_kernel(int64_t k, int sms, int64_t *body_gates);
+/* K1 dispatch, host logic only (no GPU needed): the kernel launches a fused bootstrap of k gates is split
+ * into on a device with `sms` multiprocessors.  Segment i covers gates[i] consecutive gates and runs as
+ * variants[i] = 4 (K1d, one gate per warp, warps[i] = 1..12 gates per CTA: throughput) or 5 (K1e, one gate per
+ * two-CTA cluster: latency; warps[i] = 0).  Returns the number of segments (at most 4); arrays may be NULL. */
+int tfb_debug_plan_kernels(int64_t k, int sms, int32_t *variants, int32_t *warps, int64_t *gates, int max_segments);
 
 /* Number of kernels this context has launched so far (bench `gpu_launches`). */
 int64_t tfb_kernel_launches(const tfb_ctx *ctx);

@@ -89,7 +89,8 @@ def lib() -> ctypes.CDLL:
     L.tfb_debug_blind_rotate.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     L.tfb_debug_key_switch.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
     L.tfb_debug_spectral_key.argtypes = [_vp, ctypes.c_int32, ctypes.c_int32, _vp]
-    L.tfb_debug_pick_kernel.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
+    L.tfb_debug_plan_kernels.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_int32),
+                                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
     L.tfb_kernel_launches.argtypes = [_vp]
     L.tfb_kernel_launches.restype = ctypes.c_int64
     L.tfb_measure_peaks.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -103,7 +104,7 @@ EXPORTS = (
     "tfb_abi_version", "tfb_last_error", "tfb_ctx_create", "tfb_ctx_destroy", "tfb_load_keys",
     "tfb_gate_launch", "tfb_gate_launch_host", "tfb_rows_negate", "tfb_rows_phase", "tfb_rows_encrypt",
     "tfb_debug_blind_rotate", "tfb_debug_key_switch", "tfb_debug_spectral_key",
-    "tfb_debug_pick_kernel", "tfb_kernel_launches", "tfb_measure_peaks",
+    "tfb_debug_plan_kernels", "tfb_kernel_launches", "tfb_measure_peaks",
 )
 
 
@@ -146,11 +147,12 @@ class Context:
         return int(self._lib.tfb_kernel_launches(self.handle))
 
 
-def pick_kernel(k: int, sms: int = 148) -> tuple[int, int]:
-    """(variant of the tail or of the whole launch, leading gates that run as full K1d waves)."""
-    body = ctypes.c_int64()
-    which = lib().tfb_debug_pick_kernel(int(k), int(sms), ctypes.byref(body))
-    return int(which), int(body.value)
+def plan_kernels(k: int, sms: int = 148) -> list[tuple[int, int, int]]:
+    """The kernel launches a fused bootstrap of k gates runs as: [(variant, gates per CTA, gates)], variant
+    4 = K1d (one gate per warp), 5 = K1e (one gate per two-CTA cluster; gates per CTA reported as 0)."""
+    v, w, g = (ctypes.c_int32 * 4)(), (ctypes.c_int32 * 4)(), (ctypes.c_int64 * 4)()
+    n = lib().tfb_debug_plan_kernels(int(k), int(sms), v, w, g, 4)
+    return [(int(v[i]), int(w[i]), int(g[i])) for i in range(n)]
 
 
 def measure_peaks(device: int = 0) -> dict:

@@ -53,6 +53,7 @@ struct tfb_ctx {
   int force_ks = 0;            // 0 auto, 1 = K2 (IMAD), 2 = K2t (tensor cores)
   Twiddles* d_tw = nullptr;
   uint32_t* d_ext = nullptr;   // scratch [cap][EXT_STRIDE]
+  uint32_t* d_ksn = nullptr;   // K2n partial sums + counters (KSN_SCRATCH_WORDS, zero between launches)
   int64_t ext_cap = 0;
   // buffers of the host-buffer launch path
   uint32_t* d_hx = nullptr;    // [cap][ROW_STRIDE] x, y, out back to back
@@ -64,6 +65,8 @@ struct tfb_ctx {
   int64_t launches = 0;
   int sm_count = 148;
   int force_kernel = 0;        // 0 auto, 4 = K1d (warp), 5 = K1e (cluster pair)
+  int force_warps = 0;         // 0 auto, else gates per CTA of K1d (profiling)
+  int force_wide_regs = 0;     // 1: never use the 255-register build of K1d (profiling)
   std::string err;
 };
 
@@ -145,6 +148,9 @@ __device__ __forceinline__ void bulk_load(void* dst_smem, const void* src_gmem, 
 #define TFB_K1D_WARPS 12  // 3 warps per scheduler: 168 registers each, accumulators parked in tensor memory
 #endif
 constexpr int K1D_WARPS = TFB_K1D_WARPS;
+#ifndef TFB_K1D_WAVE_TABLE  // ms per wave of K1d with 1 .. 12 gates per CTA (tools/k1_ab.py, TFB_K1D_W)
+#define TFB_K1D_WAVE_TABLE 3.33, 3.21, 3.24, 3.39, 4.85, 5.45, 5.53, 4.91, 6.64, 6.70, 6.82, 6.72
+#endif
 constexpr int K1D_THREADS = K1D_WARPS * WARP_T;
 __host__ __device__ constexpr int warp_smem(int n) {
   return WBUF_BYTES + 2 * RING_N * (int)sizeof(uint32_t) + ((n + 2) * 2 + 15) / 16 * 16;
@@ -211,6 +217,7 @@ struct WarpRing {
   uint32_t full_u32;    // shared-space address of full[0]
   int chunk;            // next chunk this warp will consume (16 m + 4 s + qc: the key is stored in that order)
   int n_chunks;
+  uint32_t consumers;   // warps of this CTA (a mid-size launch runs fewer than K1D_WARPS per SM)
 
   static __device__ __forceinline__ int slot(int s) { return s % WR_SLOTS; }
   static __device__ __forceinline__ uint32_t parity(int s) { return (uint32_t)(s / WR_SLOTS) & 1u; }
@@ -247,7 +254,7 @@ struct WarpRing {
                    : "=r"(before)
                    : "r"(smem_u32(&released[sl]))
                    : "memory");
-      if (before == (uint32_t)(K1D_WARPS - 1)) {  // last one out refills the slot
+      if (before == consumers - 1u) {  // last one out refills the slot
         released[sl] = 0;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (chunk + WR_SLOTS < n_chunks) issue(chunk + WR_SLOTS);
@@ -404,7 +411,7 @@ struct TmemTw {
   }
 };
 
-__global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
+__device__ __forceinline__ void k1d_body(
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
     const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
     const cd* __restrict__ bkw, const WarpTwiddles* __restrict__ tw_global, const FactorTables* __restrict__ ft_global,
@@ -420,13 +427,15 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
   uint32_t* acc = reinterpret_cast<uint32_t*>(mine + WBUF_BYTES);
   uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
 
-  for (int i = threadIdx.x; i < (int)(sizeof(WarpTwiddles) / sizeof(cd)); i += K1D_THREADS)
+  // warps of this CTA: K1D_WARPS in a throughput launch, fewer when a mid-size launch is spread over all SMs
+  const int nwarps = (int)blockDim.x / WARP_T;
+  for (int i = threadIdx.x; i < (int)(sizeof(WarpTwiddles) / sizeof(cd)); i += (int)blockDim.x)
     reinterpret_cast<cd*>(tw)[i] = reinterpret_cast<const cd*>(tw_global)[i];
-  for (int i = threadIdx.x; i < (int)(sizeof(FactorTables) / sizeof(cd)); i += K1D_THREADS)
+  for (int i = threadIdx.x; i < (int)(sizeof(FactorTables) / sizeof(cd)); i += (int)blockDim.x)
     reinterpret_cast<cd*>(ft)[i] = reinterpret_cast<const cd*>(ft_global)[i];
   static_assert(WR_SLOTS <= 8, "eight mbarriers + eight release counters fit the 128-byte barrier block");
   WarpRing bk{bkw, ring, bars, reinterpret_cast<uint32_t*>(bars + WR_SLOTS), smem_u32(bars), 0,
-              WCHUNKS_PER_PAIR * ((n + 1) / 2)};
+              WCHUNKS_PER_PAIR * ((n + 1) / 2), (uint32_t)nwarps};
   if (threadIdx.x == 0) {
     for (int j = 0; j < WR_SLOTS; ++j) {
       mbar_init(&bk.full[j], 1);
@@ -461,7 +470,7 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // tail CTA: surplus warps redo the last ciphertext (keeps the ring protocol uniform) but do not store
-  const int64_t want = (int64_t)blockIdx.x * K1D_WARPS + wid;
+  const int64_t want = (int64_t)blockIdx.x * nwarps + wid;
   const int64_t g = want < k ? want : k - 1;
   const uint32_t* xr = pool + (int64_t)x_rows[g] * stride;
   const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
@@ -508,6 +517,21 @@ __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(
   __syncthreads();
   if (wid == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols) : "memory");
+}
+
+#define TFB_K1D_ARGS                                                                                                  \
+  const uint32_t *__restrict__ pool, const uint8_t *__restrict__ kinds, const int32_t *__restrict__ x_rows,           \
+      const int32_t *__restrict__ y_rows, int stride, int n, uint32_t mu, const cd *__restrict__ bkw,                 \
+      const WarpTwiddles *__restrict__ tw_global, const FactorTables *__restrict__ ft_global, uint32_t *__restrict__ ext, \
+      int64_t k
+// the throughput build: up to twelve warps per CTA, 168 registers per thread
+__global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(TFB_K1D_ARGS) {
+  k1d_body(pool, kinds, x_rows, y_rows, stride, n, mu, bkw, tw_global, ft_global, ext, k);
+}
+// the same code for the mid-size launches that run at most eight warps per CTA: 255 registers per thread
+constexpr int K1D_WARPS_MID = 8;
+__global__ void __launch_bounds__(K1D_WARPS_MID * WARP_T, 1) k_gate_bootstrap_warp_mid(TFB_K1D_ARGS) {
+  k1d_body(pool, kinds, x_rows, y_rows, stride, n, mu, bkw, tw_global, ft_global, ext, k);
 }
 
 // ------------------------------------------------------------------------------------
@@ -584,6 +608,78 @@ __global__ void __launch_bounds__(KS_THREADS) k_key_switch(const uint32_t* __res
       if (tid + KS_THREADS <= n) row[tid + KS_THREADS] = v1;
     }
   }
+}
+
+// K2n: key switch of a NARROW launch (the dependent levels of adders and multiplier trees: a handful of gates).
+// There the IMAD work is nothing and the time is latency: one CTA per (group of KSN_G gates, KSN_ROWS digit rows
+// = 4 ring coefficients), every key load of the thread issued before the first use, partial sums combined with
+// integer atomics into a scratch row per gate that is zero between launches: the CTA that arrives last on the
+// group's counter reads the sums back, writes  (0, b) - sum  into the pool rows and clears scratch and counter
+// again (no separate zeroing kernel, nothing to order against the inputs).
+constexpr int KSN_G = 8;                     // gates per CTA
+constexpr int KSN_I = 4;                     // ring coefficients per CTA
+constexpr int KSN_ROWS = KSN_I * KS_T;       // 32 key rows
+constexpr int KSN_MAX_GATES = 32;            // launches up to this many gates take K2n
+constexpr int KSN_SCRATCH_WORDS = KSN_MAX_GATES * ROW_STRIDE + 64;  // sums, then one counter per gate group
+__global__ void __launch_bounds__(KS_THREADS) k_key_switch_narrow(const uint32_t* __restrict__ ext,
+                                                                  const int32_t* __restrict__ ksk,
+                                                                  uint32_t* __restrict__ pool,
+                                                                  const int32_t* __restrict__ out_rows, int stride, int n,
+                                                                  int k, uint32_t* __restrict__ scratch) {
+  __shared__ int32_t digits[KSN_ROWS][KSN_G];
+  __shared__ uint32_t arrived;
+  const int tid = threadIdx.x, i0 = blockIdx.x * KSN_I, g0 = blockIdx.y * KSN_G;
+  const int live = min(KSN_G, k - g0);
+  // all key words of this thread first: 32 rows x 2 columns in flight
+  int32_t kw0[KSN_ROWS], kw1[KSN_ROWS];
+  const int32_t* kr = ksk + (int64_t)i0 * KS_T * ROW_STRIDE;
+#pragma unroll
+  for (int r = 0; r < KSN_ROWS; ++r) {
+    kw0[r] = __ldg(kr + r * ROW_STRIDE + tid);
+    kw1[r] = __ldg(kr + r * ROW_STRIDE + tid + KS_THREADS);
+  }
+  if (tid < KSN_I * KSN_G) {
+    const int c = tid / KSN_I, ii = tid % KSN_I;
+    const uint32_t ab = (c < live ? ext[(int64_t)(g0 + c) * EXT_STRIDE + i0 + ii] : 0u) + ks_bias();
+#pragma unroll
+    for (int j = 0; j < KS_T; ++j) digits[ii * KS_T + j][c] = c < live ? ks_digit(ab, j) : 0;
+  }
+  __syncthreads();
+  int32_t acc0[KSN_G], acc1[KSN_G];
+#pragma unroll
+  for (int c = 0; c < KSN_G; ++c) acc0[c] = acc1[c] = 0;
+#pragma unroll
+  for (int r = 0; r < KSN_ROWS; ++r) {
+#pragma unroll
+    for (int c = 0; c < KSN_G; ++c) {
+      const int32_t d = digits[r][c];
+      acc0[c] += d * kw0[r];
+      acc1[c] += d * kw1[r];
+    }
+  }
+  uint32_t* sums = scratch + (int64_t)g0 * ROW_STRIDE;
+#pragma unroll
+  for (int c = 0; c < KSN_G; ++c) {
+    if (c >= live) break;
+    if (tid <= n) atomicAdd(sums + c * ROW_STRIDE + tid, (uint32_t)acc0[c]);
+    if (tid + KS_THREADS <= n) atomicAdd(sums + c * ROW_STRIDE + tid + KS_THREADS, (uint32_t)acc1[c]);
+  }
+  __threadfence();
+  __syncthreads();
+  uint32_t* counter = scratch + KSN_MAX_GATES * ROW_STRIDE + blockIdx.y;
+  if (tid == 0) arrived = atomicAdd(counter, 1u);
+  __syncthreads();
+  if (arrived != gridDim.x - 1) return;
+  __threadfence();  // last CTA of the group: every other CTA's sums are visible (they sit in L2; read them there)
+  for (int c = 0; c < live; ++c) {
+    uint32_t* row = pool + (int64_t)out_rows[g0 + c] * stride;
+    const uint32_t body = ext[(int64_t)(g0 + c) * EXT_STRIDE + RING_N];
+    for (int col = tid; col <= n; col += KS_THREADS) {
+      row[col] = (col == n ? body : 0u) - __ldcg(sums + c * ROW_STRIDE + col);
+      sums[c * ROW_STRIDE + col] = 0u;
+    }
+  }
+  if (tid == 0) *counter = 0u;
 }
 
 __global__ void k_rows_zero(uint32_t* __restrict__ pool, const int32_t* __restrict__ rows, int stride, int n) {
@@ -847,11 +943,16 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
     FactorTables hf;
     fill_factor_tables<long double>(&hf, cosl, sinl);
     e = cudaMalloc(&ctx->d_ft, sizeof(FactorTables));
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_ksn, KSN_SCRATCH_WORDS * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_ksn, 0, KSN_SCRATCH_WORDS * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemcpy(ctx->d_ft, &hf, sizeof(FactorTables), cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gate_bootstrap_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              K1D_HEADER + K1D_WARPS * warp_smem(p->n));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gate_bootstrap_warp_mid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             K1D_HEADER + K1D_WARPS_MID * warp_smem(p->n));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k1e::k_gate_bootstrap_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, k1e::smem_bytes(p->n));
   if (e == cudaSuccess)
@@ -867,6 +968,8 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
     return TFB_ERR_CUDA;
   }
   if (const char* f = getenv("TFB_FORCE_KERNEL")) ctx->force_kernel = atoi(f);  // A/B switch for profiling
+  if (const char* f = getenv("TFB_K1D_W")) ctx->force_warps = atoi(f);
+  if (const char* f = getenv("TFB_K1D_NOMID")) ctx->force_wide_regs = atoi(f);
   if (const char* f = getenv("TFB_FORCE_KS")) ctx->force_ks = atoi(f);
   *out = ctx;
   return TFB_OK;
@@ -883,6 +986,7 @@ void tfb_ctx_destroy(tfb_ctx* ctx) {
   cudaFree(ctx->d_ksk_mma);
   cudaFree(ctx->d_tw);
   cudaFree(ctx->d_ext);
+  cudaFree(ctx->d_ksn);
   cudaFree(ctx->d_hx);
   cudaFree(ctx->d_hkinds);
   cudaFree(ctx->d_hrows);
@@ -935,31 +1039,84 @@ int tfb_load_keys(tfb_ctx* ctx, const int32_t* bk, const int32_t* ksk, int on_de
 }
 
 // Cost model of the two K1 variants (ms per launch on a 148-SM B200 at n = 500, measured with
-// tools/k1_ab.py; only the ratio matters).  Both run in waves of one CTA set per SM:
-//   K1e 1 gate / 2 SMs (cluster) per wave   K1d 12 gates / SM per wave
-#ifndef TFB_K1D_WAVE_MS
-#define TFB_K1D_WAVE_MS 6.6
-#endif
+// tools/k1_ab.py; only the ratios matter).  Both run in waves of one CTA set per SM:
+//   K1e 1 gate / 2 SMs (cluster) per wave
+//   K1d w gates / SM per wave, w = 1 .. 12 warps per CTA: a launch that does not fill a 12-warp wave is spread
+//       evenly over the SMs, and a CTA with fewer warps finishes sooner (each warp shares its scheduler's
+//       FP64 pipe with fewer others): K1D_WAVE_MS[w]
 #ifndef TFB_K1E_WAVE_MS
-#define TFB_K1E_WAVE_MS 0.6
+#define TFB_K1E_WAVE_MS 0.62
 #endif
-constexpr double K1D_WAVE_MS = TFB_K1D_WAVE_MS, K1E_WAVE_MS = TFB_K1E_WAVE_MS;
-static int pick_k1(int64_t k, int sms, double* cost) {
-  const double S = (double)sms;
-  const double t_d = K1D_WAVE_MS * ceil(k / (K1D_WARPS * S)), t_e = K1E_WAVE_MS * ceil(k / floor(S / 2));
-  if (cost) *cost = t_e <= t_d ? t_e : t_d;
-  return t_e <= t_d ? 5 : 4;
+constexpr double K1E_WAVE_MS = TFB_K1E_WAVE_MS;
+constexpr double K1D_WAVE_MS[K1D_WARPS + 1] = {0.0, TFB_K1D_WAVE_TABLE};
+// A launch runs as up to four segments, each one kernel launch: (variant, gates per CTA, gates).
+struct K1Seg {
+  int which, warps;
+  int64_t gates;
+};
+static double k1e_cost(int64_t k, int sms) { return K1E_WAVE_MS * ceil((double)k / floor(sms / 2.0)); }
+// one K1d wave for k <= 12 * sms gates: the cheapest CTA width that holds them
+static double k1d_wave_cost(int64_t k, int sms, int* warps) {
+  int best = K1D_WARPS;
+  for (int w = K1D_WARPS; w >= 1 && (int64_t)w * sms >= k; --w)
+    if (K1D_WAVE_MS[w] <= K1D_WAVE_MS[best]) best = w;
+  *warps = best;
+  return K1D_WAVE_MS[best];
+}
+// cheapest single-kernel choice for k <= 12 * sms gates
+static double k1_simple(int64_t k, int sms, K1Seg* seg) {
+  int w = K1D_WARPS;
+  const double t_d = k1d_wave_cost(k, sms, &w), t_e = k1e_cost(k, sms);
+  *seg = t_e <= t_d ? K1Seg{5, 0, k} : K1Seg{4, w, k};
+  return t_e <= t_d ? t_e : t_d;
+}
+// K1 dispatch.  K1e (one gate per two-SM cluster) wins on latency, K1d (one gate per warp) on throughput: full
+// waves of twelve gates per SM first; the ragged rest (or a launch below one wave) as the cheapest of: cluster
+// waves, one K1d wave of narrower CTAs on every SM, or a balanced K1d wave (4 or 8 gates per SM: one or two warps
+// on every scheduler) followed by one of the former.  Returns the number of segments.
+static int plan_k1(int64_t k, int sms, K1Seg* seg) {
+  int nseg = 0;
+  const int64_t wave_d = (int64_t)sms * K1D_WARPS;
+  const int64_t full = k / wave_d * wave_d, rest = k - full;
+  if (full) seg[nseg++] = K1Seg{4, K1D_WARPS, full};
+  if (rest == 0) return nseg;
+  K1Seg one, head, tail;
+  double best = k1_simple(rest, sms, &one);
+  int two = 0;
+  for (int w = 4; w <= 8; w += 4) {
+    const int64_t part = (int64_t)w * sms;
+    if (rest <= part) break;
+    K1Seg t;
+    const double c = K1D_WAVE_MS[w] + k1_simple(rest - part, sms, &t);
+    if (c < best) {
+      best = c;
+      two = 1;
+      head = K1Seg{4, w, part};
+      tail = t;
+    }
+  }
+  if (two) {
+    seg[nseg++] = head;
+    seg[nseg++] = tail;
+  } else {
+    seg[nseg++] = one;
+  }
+  return nseg;
 }
 
-static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, int stride, const uint8_t* kinds,
+static int launch_k1_variant(tfb_ctx* ctx, int which, int warps, const void* pool, int stride, const uint8_t* kinds,
                              const int32_t* xr, const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
   const int n = ctx->p.n;
   if (which == 5) {  // one gate per two-CTA cluster (the kernel carries __cluster_dims__(2, 1, 1))
     k1e::k_gate_bootstrap_pair<<<(unsigned)(2 * k), k1e::THREADS, k1e::smem_bytes(n), st>>>(
         (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkf, ctx->d_tw, ctx->d_ft, ext);
   } else if (which == 4) {
-    const unsigned grid = (unsigned)((k + K1D_WARPS - 1) / K1D_WARPS);
-    k_gate_bootstrap_warp<<<grid, K1D_THREADS, K1D_HEADER + K1D_WARPS * warp_smem(n), st>>>(
+    const int w = ctx->force_warps > 0 && ctx->force_warps <= K1D_WARPS
+                      ? ctx->force_warps
+                      : (warps >= 1 && warps <= K1D_WARPS ? warps : K1D_WARPS);
+    const unsigned grid = (unsigned)((k + w - 1) / w);
+    auto kernel = (w <= K1D_WARPS_MID && !ctx->force_wide_regs) ? k_gate_bootstrap_warp_mid : k_gate_bootstrap_warp;
+    kernel<<<grid, w * WARP_T, K1D_HEADER + w * warp_smem(n), st>>>(
         (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ctx->d_ft, ext, k);
   } else {
     ctx->err = "unknown K1 variant (4 = K1d warp kernel, 5 = K1e cluster kernel)";
@@ -970,46 +1127,39 @@ static int launch_k1_variant(tfb_ctx* ctx, int which, const void* pool, int stri
   return TFB_OK;
 }
 
-// K1 dispatch.  K1e (one gate per two-SM cluster) wins on latency, K1d (one gate per warp, twelve per SM) on
-// throughput.  A large launch runs its full K1d waves first and hands the ragged rest to whichever variant
-// finishes it soonest.
-// The split decision of launch_blind_rotate: variant of the tail (or of the whole launch when *body == 0).
-static int plan_k1(int64_t k, int sms, int64_t* body) {
-  const int64_t wave_d = (int64_t)sms * K1D_WARPS;
-  const int64_t full = k / wave_d * wave_d, rest = k - full;
-  double whole = 0, tail = 0;
-  const int w_whole = pick_k1(k, sms, &whole);
-  *body = 0;
-  if (full == 0 || rest == 0) return w_whole;
-  const int w_tail = pick_k1(rest, sms, &tail);
-  if (K1D_WAVE_MS * (double)(full / wave_d) + tail >= whole) return w_whole;
-  *body = full;
-  return w_tail;
-}
-
 static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, int stride, const uint8_t* kinds, const int32_t* xr,
                                const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
   if (ctx->force_kernel)
-    return launch_k1_variant(ctx, ctx->force_kernel, pool, stride, kinds, xr, yr, ext, k, st);
-  int64_t body = 0;
-  const int w_tail = plan_k1(k, ctx->sm_count, &body);
-  if (body) {
-    int rc = launch_k1_variant(ctx, 4, pool, stride, kinds, xr, yr, ext, body, st);
+    return launch_k1_variant(ctx, ctx->force_kernel, 0, pool, stride, kinds, xr, yr, ext, k, st);
+  K1Seg seg[4];
+  const int nseg = plan_k1(k, ctx->sm_count, seg);
+  int64_t at = 0;
+  for (int i = 0; i < nseg; ++i) {
+    int rc = launch_k1_variant(ctx, seg[i].which, seg[i].warps, pool, stride, kinds + at, xr + at, yr + at,
+                               ext + at * EXT_STRIDE, seg[i].gates, st);
     if (rc) return rc;
+    at += seg[i].gates;
   }
-  return launch_k1_variant(ctx, w_tail, pool, stride, kinds + body, xr + body, yr + body, ext + body * EXT_STRIDE,
-                           k - body, st);
+  return TFB_OK;
 }
 
 static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, int stride, const int32_t* out_rows,
                              int64_t k, cudaStream_t st) {
   // K2t (tensor cores) from 96 gates up: 1.6 ms instead of 16.8 ms at 2^16 gates, 0.05 ms for anything up
-  // to ~2000 gates; below, the split IMAD kernel's 0.035 ms is the shorter latency (tools/k2_ab.py)
+  // to ~2000 gates; K2n for the narrow launches of dependent circuit levels (latency); K2 (IMAD pipe, split over
+  // the ring coefficients) in between (tools/k2_ab.py).  TFB_FORCE_KS: 1 = K2, 2 = K2t, 3 = K2n where it applies.
   const bool mma = ctx->force_ks ? ctx->force_ks == 2 : k >= 96;
   if (mma) {
     const unsigned grid = (unsigned)((k + k2t::M - 1) / k2t::M) * k2t::NTILES;
     k2t::k_key_switch_mma<<<grid, k2t::THREADS, k2t::SMEM_BYTES, st>>>(ext, ctx->d_ksk_mma, (uint32_t*)pool, out_rows,
                                                                      stride, ctx->p.n, k);
+    ctx->launches += 1;
+    TFB_CUDA(ctx, cudaGetLastError());
+    return TFB_OK;
+  }
+  if (k <= KSN_MAX_GATES && (ctx->force_ks == 0 || ctx->force_ks == 3)) {
+    k_key_switch_narrow<<<dim3(RING_N / KSN_I, (unsigned)((k + KSN_G - 1) / KSN_G)), KS_THREADS, 0, st>>>(
+        ext, ctx->d_ksk, (uint32_t*)pool, out_rows, stride, ctx->p.n, (int)k, ctx->d_ksn);
     ctx->launches += 1;
     TFB_CUDA(ctx, cudaGetLastError());
     return TFB_OK;
@@ -1192,12 +1342,16 @@ int tfb_debug_spectral_key(tfb_ctx* ctx, int32_t pair, int32_t key, double* out)
   return TFB_OK;
 }
 
-int tfb_debug_pick_kernel(int64_t k, int sms, int64_t* body_gates) {
-  int64_t body = 0;
+int tfb_debug_plan_kernels(int64_t k, int sms, int32_t* variants, int32_t* warps, int64_t* gates, int max_segments) {
   if (k < 1 || sms < 1) return 0;
-  const int which = plan_k1(k, sms, &body);
-  if (body_gates) *body_gates = body;
-  return which;
+  K1Seg seg[4];
+  const int nseg = plan_k1(k, sms, seg);
+  for (int i = 0; i < nseg && i < max_segments; ++i) {
+    if (variants) variants[i] = seg[i].which;
+    if (warps) warps[i] = seg[i].warps;
+    if (gates) gates[i] = seg[i].gates;
+  }
+  return nseg;
 }
 
 int64_t tfb_kernel_launches(const tfb_ctx* ctx) { return ctx ? ctx->launches : 0; }

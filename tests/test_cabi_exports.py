@@ -54,20 +54,25 @@ def test_unsupported_parameters_are_rejected_without_a_gpu(library):
 
 
 def test_k1_dispatch_plan(library):
-    """Host-side dispatch of the fused bootstrap (no GPU): latency kernel for narrow launches, the
-    warp-per-gate kernel for wide ones, full K1d waves + a cheaper tail for ragged wide launches."""
-    pick = _cabi.pick_kernel
-    assert pick(1) == (5, 0) and pick(2) == (5, 0) and pick(74) == (5, 0)    # adders / multiplier trees: one gate per 2-SM cluster
-    assert pick(148) == (5, 0) and pick(592)[0] == 5                          # a few cluster waves still beat one warp-kernel wave
-    assert pick(1776) == (4, 0) and pick(3552) == (4, 0)                      # full waves of 12-gate CTAs
-    which, body = pick(1 << 16)                                               # BASELINE configs[1]
-    assert body in (0, 36 * 1776) and (body or which == 4)
-    which, body = pick(2 * 1776 + 30)                                         # ragged: K1d waves, then a short tail on the clusters
-    assert body == 2 * 1776 and which == 5
-    for k in (1, 7, 149, 297, 600, 1000, 1777, 5000, 100000):
-        which, body = pick(k)
-        assert which in (4, 5) and 0 <= body < k and body % 1776 == 0
-    assert pick(1776 // 2, sms=74) == (4, 0)                                  # scales with the SM count
+    """Host-side dispatch of the fused bootstrap (no GPU): the cluster kernel for narrow launches, the
+    warp-per-gate kernel spread evenly over the SMs for mid-size ones, full twelve-gate waves plus the cheapest
+    tail for wide ones."""
+    plan = _cabi.plan_kernels
+    assert plan(1) == [(5, 0, 1)] and plan(2) == [(5, 0, 2)] and plan(74) == [(5, 0, 74)]  # adders / multiplier trees
+    assert plan(148) == [(5, 0, 148)]                       # two cluster waves beat one warp-kernel wave
+    assert plan(592) == [(4, 4, 592)]                       # one warp on every scheduler of every SM
+    assert plan(1184) == [(4, 8, 1184)] and plan(1776) == [(4, 12, 1776)] and plan(3552) == [(4, 12, 3552)]
+    segs = plan(1 << 16)                                    # BASELINE configs[1]: 36 full waves, then the rest
+    assert segs[0] == (4, 12, 36 * 1776) and sum(g for _, _, g in segs) == 1 << 16
+    assert plan(2 * 1776 + 30) == [(4, 12, 2 * 1776), (5, 0, 30)]  # ragged: a short tail on the clusters
+    for k in (1, 7, 149, 297, 600, 700, 1000, 1777, 2500, 5000, 100000):
+        segs = plan(k)
+        assert 1 <= len(segs) <= 4 and sum(g for _, _, g in segs) == k
+        for which, warps, gates in segs:
+            assert gates > 0 and ((which == 5 and warps == 0) or (which == 4 and 1 <= warps <= 12))
+            if which == 4:
+                assert gates <= 148 * warps or warps == 12  # a narrower wave fits the chip once
+    assert plan(1776 // 2, sms=74) == [(4, 12, 888)]        # scales with the SM count
 
 
 def test_product_path_never_touches_the_oracle():

@@ -141,6 +141,40 @@ def test_every_kernel_variant_is_bit_exact(key, eval_keys, monkeypatch):
         ctx.close()
 
 
+def test_k1d_cta_widths_are_bit_exact(key, eval_keys, monkeypatch):
+    """K1d with 1 .. 12 gates per CTA (a mid-size launch is spread over all SMs with fewer warps per CTA; up to
+    eight warps run the 255-register build of the same code): every width, both builds, ragged last CTA."""
+    import torch
+
+    from paper_2005_01945_b200 import _cabi
+
+    xs, ys, kinds, bits = make_inputs(key, 29, seed=37, kinds=(np.arange(29) % 9).astype(np.uint8))
+    want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
+    monkeypatch.setenv("TFB_FORCE_KERNEL", "4")
+    for warps, nomid in ((1, 0), (2, 0), (3, 1), (4, 0), (5, 0), (7, 1), (8, 0), (8, 1), (9, 0), (11, 0)):
+        monkeypatch.setenv("TFB_K1D_W", str(warps))
+        monkeypatch.setenv("TFB_K1D_NOMID", str(nomid))
+        ctx = _cabi.Context(0, key.params.m, key.params.mu.word, eval_keys.ring)
+        ctx.call("tfb_load_keys", eval_keys.bk.ctypes.data, eval_keys.ksk.ctypes.data, 0, None)
+        got = run_launch((ctx, torch, _cabi), key, xs, ys, kinds)
+        assert np.array_equal(got, want), f"{warps} gates per CTA, 168-register build forced: {nomid}"
+        ctx.close()
+
+
+def test_planned_segments_are_bit_exact(gpu, key, eval_keys):
+    """A launch the dispatch splits into a K1d wave of narrow CTAs plus a cluster-kernel tail (700 gates on 148
+    SMs) gives the same words as the oracle, segment boundaries included."""
+    from paper_2005_01945_b200 import _cabi
+
+    k = 700
+    segs = _cabi.plan_kernels(k, 148)
+    xs0, ys0, kinds0, _ = make_inputs(key, 20, seed=38, kinds=(np.arange(20) % 9).astype(np.uint8))
+    want0 = orc.gate_bootstrap_batch(xs0, ys0, kinds0, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
+    idx = np.arange(k) % 20
+    got = run_launch(gpu, key, xs0[idx], ys0[idx], kinds0[idx])
+    assert np.array_equal(got, want0[idx]), segs
+
+
 def test_key_switch_on_tensor_cores_is_exact(key, eval_keys, monkeypatch):
     """K2t (tcgen05.mma kind::i8: digits x byte planes of the key, s32 accumulators in tensor memory)
     against K2 (IMAD pipe) on arbitrary extracted samples, whole and partial 128-gate tiles, and against
@@ -179,6 +213,25 @@ def test_key_switch_on_tensor_cores_is_exact(key, eval_keys, monkeypatch):
             want = (-(digits[:, None] * ksk.astype(np.int64)).sum(axis=0)) % (1 << 32)
             want[n] = (want[n] + int(ext_h[g, 1024])) % (1 << 32)
             assert np.array_equal(outs["2"][int(rows[g].item()), : n + 1].astype(np.int64), want), (K, g)
+    # K2n, the narrow-launch kernel (partial sums combined by atomics in a self-cleaning scratch, last CTA writes
+    # the rows): every group shape up to its 32-gate limit, twice in a row (the scratch must come back clean)
+    monkeypatch.setenv("TFB_FORCE_KS", "3")
+    ctxs["3"] = _cabi.Context(0, n, key.params.mu.word, eval_keys.ring)
+    ctxs["3"].call("tfb_load_keys", eval_keys.bk.ctypes.data, eval_keys.ksk.ctypes.data, 0, None)
+    for K in (1, 2, 7, 8, 9, 29, 32, 3):
+        ext_h = rng.integers(0, 1 << 32, size=(K, _cabi.EXT_STRIDE), dtype=np.uint32)
+        ext_h[K - 1, :1024] = 0xFFFFFFFF
+        ext = torch.from_numpy(ext_h.view(np.int32)).to(dev)
+        rows = torch.arange(K, dtype=torch.int32, device=dev).flip(0).contiguous()
+        outs = {}
+        for mode in ("1", "3", "3 again"):
+            pool = torch.full((K, _cabi.ROW_STRIDE), 7, dtype=torch.int32, device=dev)
+            ctxs[mode[0]].call("tfb_debug_key_switch", ext.data_ptr(), pool.data_ptr(), rows.data_ptr(), K, None)
+            torch.cuda.synchronize()
+            outs[mode] = pool.cpu().numpy().view(np.uint32)
+        assert np.array_equal(outs["1"][:, : n + 1], outs["3"][:, : n + 1]), K
+        assert np.array_equal(outs["3"], outs["3 again"]), K
+        assert (outs["3"][:, n + 1 :] == 7).all()  # nothing outside the n + 1 words of a row is written
     for ctx in ctxs.values():
         ctx.close()
 
@@ -213,7 +266,7 @@ def test_automatic_dispatch_sizes(gpu, key, eval_keys):
     base = 64
     xs, ys, kinds, bits = make_inputs(key, base, seed=37)
     want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
-    for K in (1, 2, 297, 889, 1030, 1775, 1777, 1800):
+    for K in (1, 2, 33, 297, 400, 889, 1030, 1775, 1777, 1800, 2500):
         idx = np.arange(K) % base
         got = run_launch(gpu, key, xs[idx], ys[idx], kinds[idx])
         assert np.array_equal(got, want[idx]), K
