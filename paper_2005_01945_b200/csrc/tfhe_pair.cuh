@@ -77,9 +77,8 @@ TFB_HD void pair_combine_keys(Env& env, const uint16_t* abar, int n, int m, uint
     for (int k4 = 0; k4 < 4; ++k4) {
       const int k2 = 4 * h + k4;
       // X^a at point cl + 256 k2: base * exp(i pi a 256 k2 / N) = base * A[8 a k2 mod 64]
-      cd u1 = cmul(base1, ft->A[(8 * a1 * k2) & 63]), u2 = cmul(base2, ft->A[(8 * a2 * k2) & 63]);
-      u1.re -= 1.0;
-      u2.re -= 1.0;
+      const cd u1 = rotation_minus_one(base1, ft->A[(8 * a1 * k2) & 63]);
+      const cd u2 = rotation_minus_one(base2, ft->A[(8 * a2 * k2) & 63]);
       keep[k2 * STRIDE] = combine_keys(u1, u2, chunk[pchunk_index(k4, 0, c_keep, t)], chunk[pchunk_index(k4, 1, c_keep, t)],
                                        chunk[pchunk_index(k4, 2, c_keep, t)]);
       give[k2 * STRIDE] = combine_keys(u1, u2, chunk[pchunk_index(k4, 0, c_keep ^ 1, t)],
@@ -140,12 +139,11 @@ TFB_HD void pair_blind_rotate(Env& env, int n, const Twiddles* tw, const FactorT
     env.cta_sync();
     env.key_done(1, m, 1);
   }
+  if (tid == 0 && m < pairs) env.arm_recv(0);
 #if defined(__CUDA_ARCH__)
 #pragma unroll 1
 #endif
   while (m < pairs) {  // uniform across the cluster: both CTAs derive the same rotations
-    const int m_next = pair_next_active(abar, n, m + 1);
-    if (tid == 0) env.arm_recv(step);
     env.tick(0);
     cd x[8];
 #pragma unroll
@@ -192,7 +190,12 @@ TFB_HD void pair_blind_rotate(Env& env, int n, const Twiddles* tw, const FactorT
       }
     }
     env.tick(5);
-    if (!Env::helpers && m_next < pairs)  // while the peer's words travel
+    // bookkeeping of the next step while the peer's words travel: the next active pair, and the receive barrier of
+    // step + 1 (the other buffer; its previous phase ended with step - 1's data, and a transfer that completed
+    // before its expect_tx would only leave the transaction count negative for a while)
+    const int m_next = pair_next_active(abar, n, m + 1);
+    if (tid == 0 && m_next < pairs) env.arm_recv(step + 1);
+    if (!Env::helpers && m_next < pairs)
       pair_combine_keys<1>(env, abar, n, m_next, 2 * (step + 1), ft, p, grp, t, kk, kg);
     env.tick(6);
     if (grp == 0) {

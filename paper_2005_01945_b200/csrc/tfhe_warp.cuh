@@ -511,23 +511,12 @@ TFB_HD void wmac(Park& park, const cd* x, BkSource& bk, int m, int s, const Pair
 #pragma unroll
     for (int j = 0; j < PARK_CH; ++j) {
       const int q = qb + j;
-      cd u1 = cmul(pf.base1, ft->A[(4 * pf.a1 * q) & 63]), u2 = cmul(pf.base2, ft->A[(4 * pf.a2 * q) & 63]);
-      u1.re -= 1.0;
-      u2.re -= 1.0;
-#if defined(TFB_X_NOKEYS)  // timing-only experiment (wrong results): no key loads at all, same FP64 work
-      const cd k0 = combine_keys(u1, u2, x[(q + 1) & 15], x[(q + 2) & 15], x[(q + 3) & 15]);
-      const cd k1 = combine_keys(u2, u1, x[(q + 4) & 15], x[(q + 5) & 15], x[(q + 6) & 15]);
-#elif defined(TFB_X_HALFKEYS)  // timing-only experiment (wrong results): half of the key loads, same FP64 work
-      const cd k0 = combine_keys(u1, u2, bk.load(key + wchunk_index(j, 0, 0, 0)), bk.load(key + wchunk_index(j, 1, 0, 0)),
-                                 bk.load(key + wchunk_index(j, 2, 0, 0)));
-      const cd k1 = combine_keys(u2, u1, bk.load(key + wchunk_index(j, 1, 0, 0)), bk.load(key + wchunk_index(j, 0, 0, 0)),
-                                 bk.load(key + wchunk_index(j, 2, 0, 0)));
-#else
+      const cd u1 = rotation_minus_one(pf.base1, ft->A[(4 * pf.a1 * q) & 63]);
+      const cd u2 = rotation_minus_one(pf.base2, ft->A[(4 * pf.a2 * q) & 63]);
       const cd k0 = combine_keys(u1, u2, bk.load(key + wchunk_index(j, 0, 0, 0)), bk.load(key + wchunk_index(j, 1, 0, 0)),
                                  bk.load(key + wchunk_index(j, 2, 0, 0)));
       const cd k1 = combine_keys(u1, u2, bk.load(key + wchunk_index(j, 0, 1, 0)), bk.load(key + wchunk_index(j, 1, 1, 0)),
                                  bk.load(key + wchunk_index(j, 2, 1, 0)));
-#endif
       if (FIRST) {
         o0[j] = cmul(x[q], k0);
         o1[j] = cmul(x[q], k1);
