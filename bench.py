@@ -750,8 +750,9 @@ def run_b200(args) -> None:
         with open(prof) as f:
             rec = json.load(f)
         traffic = rec.get("dram_bytes_per_launch")
-        traffic_src = ("stored ncu --set full capture of this kernel at 2**16 gates (dram__bytes_read.sum + "
-                       f"dram__bytes_write.sum), {rec.get('source', 'profiles/')}; not re-measured in this run")
+        traffic_src = (f"stored ncu --set full capture of this kernel at {rec.get('gates_per_launch')} gates per launch "
+                       f"(dram__bytes_read.sum + dram__bytes_write.sum), {rec.get('source', 'profiles/')}; "
+                       "not re-measured in this run")
     line = {
         "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": job.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
