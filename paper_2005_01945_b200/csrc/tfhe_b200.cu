@@ -4,12 +4,16 @@
 //   K1 fused gate linear form + mod switch + blind rotation + sample extract.  The bootstrapping key is
 //      UNROLLED over pairs of LWE mask elements (three TRGSW samples per pair, ceil(n/2) steps of four forward
 //      and two inverse FP64 negacyclic transforms); ACC resident in shared memory:
-//      K1d k_gate_bootstrap_warp  one gate per WARP, twelve per SM, spectral key staged by TMA through a
-//                                 release-count ring, accumulators parked in tensor memory (tfhe_warp.cuh)
+//      K1d k_gate_bootstrap_warp  one gate per WARP, up to twelve per SM, spectral key staged by TMA through a
+//                                 release-count ring, accumulators parked in tensor memory (tfhe_warp.cuh);
+//                                 k_gate_bootstrap_warp_mid: the same code for up to eight warps per CTA (255
+//                                 registers), what a mid-size launch spread over all SMs runs
 //      K1e k_gate_bootstrap_pair  one gate per two-CTA cluster, one accumulator polynomial per SM, DSMEM
 //                                 exchange (latency path; tfhe_pair.cuh + tfhe_cluster.cuh)
 //   K2 k_key_switch       batched N -> n key switch as an integer rank-8192 update,
-//                         32 ciphertexts x 512 columns per CTA, digits in smem (launches < 96 gates)
+//                         32 ciphertexts x 512 columns per CTA, digits in smem (launches of 33 .. 95 gates)
+//   K2n k_key_switch_narrow  the same for launches of up to 32 gates (dependent circuit levels): all loads in
+//                         flight, partial sums by atomics into a self-cleaning scratch, last CTA writes the rows
 //   K2t k_key_switch_mma  the same update as an exact s8 x u8 -> s32 GEMM on the tensor cores
 //                         (tcgen05.mma kind::i8, TMEM accumulator), tfhe_keyswitch_mma.cuh
 //   K3 k_bk_transform(_w) one-time: raw TRGSW rows -> spectral key in K1e's / K1d's chunk order;
