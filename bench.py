@@ -266,7 +266,8 @@ def reference_circuit_seconds(workers_list=None) -> dict | None:
         for n in (16, 32):
             a, b = (int(v) for v in rng.integers(0, 1 << n, size=2, dtype=np.uint64))
             x, y = encirc.encrypt_int(eng, a, n), encirc.encrypt_int(eng, b, n)
-            for name, fn, want in ((f"add{n}", encirc.add_bitwise, (a + b) % (1 << n)), (f"mul{n}", encirc.mul_naive, a * b)):
+            for name, fn, want in ((f"add{n}", encirc.add_bitwise, (a + b) % (1 << n)), (f"mul{n}", encirc.mul_naive, a * b),
+                                   (f"karatsuba{n}", encirc.mul_karatsuba, a * b)):
                 best = None
                 for _ in range(3):
                     t0 = time.perf_counter()
@@ -488,6 +489,27 @@ def gates_workload(job: Job) -> dict:
             reps = 3 if kk >= 4096 else 10
             sweep[str(kk)] = kk * reps / (job.timed(part, reps) * 1e-3)
 
+    # configs[1] also names AND / XOR launches and a 50/50 XOR + AND compound mix (a compound launch interleaves the
+    # two kinds over the same input pairs, encirc/engine.py:300-320): same launch size, one timed launch each
+    by_kind = {}
+    if job.rank == 0 and job.world == 1:
+        pairs = k // 2
+        for name, kind_ids in (("AND", np.full(k, 0, np.uint8)), ("XOR", np.full(k, 4, np.uint8)),
+                               ("XOR+AND compound mix", np.tile(np.array([4, 0], np.uint8), pairs))):
+            kd = torch.from_numpy(kind_ids).to(dev)
+            if name.endswith("mix"):  # jobs 2i and 2i+1 share the input pair i
+                xi = torch.arange(pairs, dtype=torch.int32, device=dev).repeat_interleave(2)
+                xm, ym = xi.contiguous(), (xi + k).contiguous()
+            else:
+                xm, ym = xr, yr
+
+            def part(kd=kd, xm=xm, ym=ym):
+                ctx.call("tfb_gate_launch", pool.data_ptr(), kd.data_ptr(), xm.data_ptr(), ym.data_ptr(), orow.data_ptr(),
+                         len(kd), job.stream)
+
+            part()
+            by_kind[name] = len(kd) / (job.timed(part, 1) * 1e-3)
+
     # dominant kernel alone (K1: fused blind rotation) for the roofline
     ext = torch.empty((k, _cabi.EXT_STRIDE), dtype=torch.int32, device=dev)
 
@@ -524,7 +546,7 @@ def gates_workload(job: Job) -> dict:
     del pool
     return {
         "value": value, "ms_per_step": total_ms / args.steps, "scaling": "weak", "clocks": clocks.summary(),
-        "gpu_launches": int(gpu_launches), "correct": correct, "k1_ms": k1_ms, "sweep": sweep,
+        "gpu_launches": int(gpu_launches), "correct": correct, "k1_ms": k1_ms, "sweep": sweep, "by_kind": by_kind,
         "e2e": {"value": job.world * k * e2e_steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int(2 * k * (n + 1) * 4 + k), "d2h_bytes_per_step": int(k * (n + 1) * 4),
                 "api": "tfb_gate_launch_host (C ABI, pinned host buffers)", "correct": e2e_ok},
@@ -647,7 +669,7 @@ def time_circuits(job: Job) -> dict:
     2n+1 / ~138 dependent kernel-launch levels) and throughput of a batch of independent operations (vec_add /
     vec_mul lanes), each beside the reference's CPU engine timed in this run."""
     from paper_2005_01945_b200 import (
-        add_bitwise, decrypt_int, decrypt_vector, encrypt_int, encrypt_vector, mul_naive, vec_add, vec_mul,
+        add_bitwise, decrypt_int, decrypt_vector, encrypt_int, encrypt_vector, mul_karatsuba, mul_naive, vec_add, vec_mul,
     )
 
     eng = job.eng
@@ -656,7 +678,8 @@ def time_circuits(job: Job) -> dict:
     for n in (16, 32):
         a, b = (int(v) for v in rng.integers(0, 1 << n, size=2, dtype=np.uint64))
         x, y = encrypt_int(eng, a, n), encrypt_int(eng, b, n)
-        for name, fn, want in ((f"add{n}", add_bitwise, (a + b) % (1 << n)), (f"mul{n}", mul_naive, a * b)):
+        for name, fn, want in ((f"add{n}", add_bitwise, (a + b) % (1 << n)), (f"mul{n}", mul_naive, a * b),
+                               (f"karatsuba{n}", mul_karatsuba, a * b)):
             fn(encrypt_int(eng, 3, n), encrypt_int(eng, 5, n))  # warm the launch path (first use of each kernel variant)
             eng.synchronize()
             best = None
@@ -690,7 +713,7 @@ def time_circuits(job: Job) -> dict:
     else:
         out["reference_cpu"] = cpu
         ratios = {}
-        for name in ("add16", "mul16", "add32", "mul32", "add32_x256", "mul32_x16"):
+        for name in ("add16", "mul16", "karatsuba16", "add32", "mul32", "karatsuba32", "add32_x256", "mul32_x16"):
             best_cpu = min(cpu[w][name]["seconds"] for w in cpu if w.startswith("workers_"))
             ratios[name] = best_cpu / out[name]["seconds"]
         out["speedup_vs_reference_cpu"] = ratios  # > 1: the GPU finishes sooner than the reference's CPU oracle engine
@@ -777,7 +800,8 @@ def run_b200(args) -> None:
         if extra in head:
             line[extra] = head[extra]
     if head.get("sweep"):
-        line["sweep"] = {"unit": UNIT, "gates_per_s_by_launch_size": head["sweep"]}
+        line["sweep"] = {"unit": UNIT, "gates_per_s_by_launch_size": head["sweep"],
+                         "gates_per_s_by_kind_at_full_launch": head.get("by_kind", {})}
     if sharded is not None:
         line["sharded"] = sharded
     if job.world == 1 and not args.no_cpu_baseline:
