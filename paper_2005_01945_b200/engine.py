@@ -236,6 +236,7 @@ class GateEngine:
         self._deferred: dict = {}          # level -> launches counted but not yet executed (lazy engines only)
         self._deferred_gates = 0
         self._deferred_launches = 0
+        self._depth_done = 0               # highest level of the current queue epoch already handed to the device
         self._row_level = np.zeros(1024, dtype=np.int32)  # level of the queued launch that will write a row (0: none)
         self.physical_launches = 0         # _evaluate calls (logical launches are stats.batch_launches)
 
@@ -458,37 +459,60 @@ class GateEngine:
             grown = np.zeros(len(self._bounds), dtype=np.int32)
             grown[: len(self._row_level)] = self._row_level
             self._row_level = grown
-        level = 1
+        # levels are absolute depths of the current queue epoch: levels up to _depth_done have already been handed
+        # to the device (early start, below), so a launch whose inputs are all evaluated joins the next one to run
+        level = self._depth_done + 1
         if self._deferred:
             lv = self._row_level
-            level += int(max(lv[x_rows].max(), lv[y_rows].max()))
+            level = max(level, 1 + int(max(lv[x_rows].max(), lv[y_rows].max())))
         self._alloc.hold = True  # rows freed from now on may still be read or written by the queue
         self._deferred.setdefault(level, []).append((np.array(kind_ids, np.uint8), x_rows, y_rows, out_rows))
         self._deferred_gates += k
         self._deferred_launches += 1
         self._row_level[out_rows] = level
+        self._early_start()
+
+    def _early_start(self) -> None:
+        """Hook: an engine whose device would otherwise idle while a circuit is still being recorded may hand the
+        lowest queued level over now (`_run_next_level`).  Default: nothing runs before something reads a row."""
+
+    def _run_next_level(self) -> None:
+        """Execute the lowest queued level as one kernel launch; everything above it stays queued."""
+        level = min(self._deferred)
+        batch = self._deferred.pop(level)
+        gates = sum(len(q[0]) for q in batch)
+        try:
+            if len(batch) == 1:
+                kinds, xs, ys, outs = batch[0]
+            else:
+                kinds, xs, ys, outs = (np.concatenate([q[j] for q in batch]) for j in range(4))
+            self.physical_launches += 1
+            self._evaluate(kinds, xs, ys, outs)
+        finally:
+            for q in batch:
+                self._row_level[q[3]] = 0
+            self._deferred_gates -= gates
+            self._deferred_launches -= len(batch)
+            self._depth_done = level
+            if not self._deferred:  # the epoch is over: depths start again, quarantined rows go back to the allocator
+                self._depth_done = 0
+                self._alloc.end_hold()
 
     def _run_deferred(self) -> None:
         """Execute the queue, one kernel launch per level.  Called before anything reads or rewrites rows."""
-        if not self._deferred:
-            return
-        queue, self._deferred = self._deferred, {}
-        self._deferred_gates = self._deferred_launches = 0
         try:
-            for level in sorted(queue):
-                batch = queue[level]
-                if len(batch) == 1:
-                    kinds, xs, ys, outs = batch[0]
-                else:
-                    kinds, xs, ys, outs = (np.concatenate([q[j] for q in batch]) for j in range(4))
-                self.physical_launches += 1
-                self._evaluate(kinds, xs, ys, outs)
-                self._row_level[outs] = 0
-        finally:
-            for batch in queue.values():  # after an error nothing may stay marked as pending
+            while self._deferred:
+                self._run_next_level()
+        except BaseException:
+            # after an error nothing may stay marked as pending
+            for batch in self._deferred.values():
                 for q in batch:
                     self._row_level[q[3]] = 0
+            self._deferred = {}
+            self._deferred_gates = self._deferred_launches = 0
+            self._depth_done = 0
             self._alloc.end_hold()
+            raise
 
     def bootstrap(self, bit: EncBit) -> EncBit:
         """Standalone refresh; precondition noise_bound < mu, one launch."""
@@ -657,6 +681,8 @@ class B200Engine(GateEngine):
         self._pool_t = torch.zeros((initial_rows, _cabi.ROW_STRIDE), dtype=torch.int32, device=self.device)
         self._pending: list = []  # (first row, packed host words) awaiting upload
         self._stage = None
+        self._submits = 0
+        self._inflight: list = []  # completion events of levels handed to the device ahead of a flush
         super().__init__(key.params, pool)
         self._enc_rng = np.random.default_rng((self.seed, self._ENC_STREAM))
         # device_encrypt: fresh encryptions drawn on the GPU by a counter-based generator (throughput inputs:
@@ -695,6 +721,9 @@ class B200Engine(GateEngine):
         """Bring device storage up to date: queued launches first (their inputs' uploads happen inside),
         then host words waiting for upload."""
         self._run_deferred()
+        self._upload_pending()
+
+    def _upload_pending(self) -> None:
         if not self._pending:
             return
         torch, n1 = self._torch, self.params.m + 1
@@ -714,27 +743,56 @@ class B200Engine(GateEngine):
 
     def _stage_small(self, kind_ids, x_rows, y_rows, out_rows):
         """Index arrays + kinds of a narrow launch in ONE host->device copy from pinned memory (the latency path issues
-        a launch per gate level: two pageable copies per level were ~5 % of a level).  Staging slots rotate, so a slot
-        is rewritten long after the copy that read it was ordered before later work on the stream."""
+        a launch per gate level: two pageable copies per level were ~5 % of a level).  Staging slots rotate; each carries
+        the event of its last copy."""
         torch, k = self._torch, len(kind_ids)
         if self._stage is None:
             words = 4 * self.STAGE_GATES  # x, y, out (int32 each) + kinds (uint8, padded to a word each 4)
             self._stage = [(torch.empty(words, dtype=torch.int32).pin_memory(),
-                            torch.empty(words, dtype=torch.int32, device=self.device)) for _ in range(8)]
+                            torch.empty(words, dtype=torch.int32, device=self.device),
+                            torch.cuda.Event()) for _ in range(16)]
             self._stage_at = 0
-        host, dev = self._stage[self._stage_at]
+            self._stage_used = 0
+        host, dev, copied = self._stage[self._stage_at]
         self._stage_at = (self._stage_at + 1) % len(self._stage)
-        if self._stage_at == 0:
-            torch.cuda.current_stream(self.device).synchronize()  # every slot's last copy has completed before reuse
+        if self._stage_used >= len(self._stage):
+            # the pinned half of a slot may be rewritten once ITS last copy has run (sixteen launches ago: long done);
+            # the device half is protected by stream order.  No stream-wide wait: the queue of levels stays full.
+            copied.synchronize()
+        self._stage_used += 1
         h = host.numpy()
         h[:k], h[k : 2 * k], h[2 * k : 3 * k] = x_rows, y_rows, out_rows
         h[3 * k : 3 * k + (k + 3) // 4].view(np.uint8)[:k] = kind_ids
         n = 3 * k + (k + 3) // 4
         dev[:n].copy_(host[:n], non_blocking=True)
+        copied.record(torch.cuda.current_stream(self.device))
         return dev.data_ptr(), dev.data_ptr() + 12 * k
 
+    # Early start: a circuit is recorded launch by launch (~20 us of Python each: 19 ms for a 32-bit multiply) before
+    # anything reads a result, and the device would idle meanwhile.  Every eighth recorded launch the engine looks at
+    # the device; while fewer than two handed-over levels are still in flight it hands over the lowest queued level.
+    # Levels are absolute depths (GateEngine._submit), so launches recorded later simply join the next level to run.
+    EARLY_START = os.environ.get("TFB_EARLY_START", "1") not in ("", "0")
+    EARLY_START_EVERY = 8
+    EARLY_START_IN_FLIGHT = 2
+
+    def _early_start(self) -> None:
+        if not self.EARLY_START:
+            return
+        self._submits += 1
+        if self._submits % self.EARLY_START_EVERY:
+            return
+        inflight = self._inflight
+        while inflight and inflight[0].query():
+            inflight.pop(0)
+        if len(inflight) < self.EARLY_START_IN_FLIGHT and self._deferred:
+            self._run_next_level()
+            done = self._torch.cuda.Event()
+            done.record(self._torch.cuda.current_stream(self.device))
+            inflight.append(done)
+
     def _evaluate(self, kind_ids, x_rows, y_rows, out_rows) -> None:
-        self._flush()
+        self._upload_pending()  # (not _flush: the queue above this level stays queued)
         k = len(kind_ids)
         if k <= self.STAGE_GATES:
             base, kinds_ptr = self._stage_small(kind_ids, x_rows, y_rows, out_rows)

@@ -121,3 +121,43 @@ def test_not_bootstrap_and_margin_errors_with_queued_launches(small_key):
         with pytest.raises(BootstrapMarginError):          # raised at the call, not when the queue runs
             eng.eval_gate(GateKind.AND, noisy, a)
         assert eng.decrypt(eng.eval_gate(GateKind.XOR, a, b)) == 1
+
+
+class _EarlyStarter(HostOracleEngine):
+    """A lazy host engine that hands the lowest queued level over every `every` recorded launches, the way
+    B200Engine does while its device would otherwise idle."""
+
+    every = 3
+
+    def _early_start(self):
+        self._seen = getattr(self, "_seen", 0) + 1
+        if self._seen % self.every == 0 and self._deferred:
+            self._run_next_level()
+
+
+@pytest.mark.parametrize("every", [1, 2, 5, 17])
+def test_early_start_is_unobservable(small_key, every):
+    """Levels handed to the device while the circuit is still being recorded (absolute level numbering: a launch
+    whose inputs are already evaluated joins the next level to run): results, ciphertext words, statistics and row
+    recycling are those of the eager engine, and the dependent chain does not grow beyond the eager one."""
+    pool = lambda: WorkerPool(PoolConfig(workers=1, max_batch=1 << 16))
+    eager = HostOracleEngine(small_key, seed=3, pool=pool(), lazy=False)
+    early = _EarlyStarter(small_key, seed=3, pool=pool(), lazy=True)
+    early.every = every
+    early.eval_keys = eager.eval_keys
+    got = {}
+    for eng in (eager, early):
+        x, y = encrypt_int(eng, 0xC5, 8), encrypt_int(eng, 0x3B, 8)
+        eng.reset_stats()
+        eng.physical_launches = 0
+        p = mul_naive(x, y)
+        s = add_bitwise(x, y)
+        gc.collect()
+        v = vec_add(encrypt_vector(eng, [9, 130], 8), encrypt_vector(eng, [250, 7], 8))
+        got[eng is early] = (decrypt_int(eng, p), decrypt_int(eng, s), decrypt_vector(eng, v), eng.stats.as_record(),
+                             eng.read_rows([b.row for b in p.bits] + [b.row for b in s.bits]), eng.physical_launches)
+        assert not eng._deferred and eng._depth_done == 0 and not eng._alloc.hold
+    assert got[True][:4] == got[False][:4]
+    assert got[False][0] == 0xC5 * 0x3B and got[False][1] == (0xC5 + 0x3B) % 256 and got[False][2] == [3, 137]
+    assert np.array_equal(got[True][4], got[False][4])
+    assert got[True][5] <= got[False][5]
