@@ -40,8 +40,16 @@ constexpr int OFF_SWAP = OFF_XBUF + 2 * 2 * HALF_N * (int)sizeof(cd);         //
 constexpr int OFF_ACC = OFF_SWAP + 2 * HALF_N * (int)sizeof(cd);              // N words
 constexpr int OFF_RECV = OFF_ACC + RING_N * 4;                                // 2 buffers x N words
 constexpr int OFF_FT = OFF_RECV + 2 * RECV_WORDS * 4;                         // FactorTables
-constexpr int OFF_BARS = OFF_FT + (int)sizeof(FactorTables);                  // 2 receive + 2 x 2 ring mbarriers
-constexpr int OFF_ABAR = OFF_BARS + 64;
+// mbarriers: RECV_BARS receive barriers per step parity (the peer's 4 KB is accounted on several barriers: every
+// st.async completes 16 bytes of transaction count on its barrier, and 256 of them on ONE barrier serialise), then
+// 2 x 2 ring barriers
+#ifndef TFB_K1E_RECV_BARS
+#define TFB_K1E_RECV_BARS 2
+#endif
+constexpr int RECV_BARS = TFB_K1E_RECV_BARS;
+static_assert(RECV_BARS == 1 || RECV_BARS == 2 || RECV_BARS == 4, "one barrier per st.async of a thread, or fewer");
+constexpr int OFF_BARS = OFF_FT + (int)sizeof(FactorTables);
+constexpr int OFF_ABAR = OFF_BARS + 128;
 __host__ __device__ constexpr int smem_bytes(int n) { return OFF_ABAR + ((n + 2) * 2 + 15) / 16 * 16; }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -105,7 +113,7 @@ struct DeviceEnv {
   const cd* bkf;        // spectral key in global memory (pchunk layout)
   cd* ring;             // this gadget level's two slots
   cd* keys;             // combined-key blocks [buffer][group][keep / give][k2][t]
-  uint32_t bars_local;  // shared-space address of the CTA's mbarriers: [0,1] receive, [2 + 2 grp + slot] ring
+  uint32_t bars_local;  // shared-space address of the CTA's mbarriers: [parity * RECV_BARS + j] receive, then [2 grp + slot] ring
   uint32_t recv_local, recv_peer, bars_peer;
   const uint16_t* abar;
   int n, p, grp, t, tid;
@@ -115,7 +123,7 @@ struct DeviceEnv {
   __device__ __forceinline__ void cta_sync() { asm volatile("bar.sync %0, %1;" ::"n"(BAR_MAIN_CTA), "n"(PAIR_THREADS) : "memory"); }
   __device__ __forceinline__ void all_sync() { __syncthreads(); }
   __device__ __forceinline__ uint32_t ring_bar(uint32_t seq) const {
-    return bars_local + 8u * (2u + (uint32_t)RING_SLOTS * (uint32_t)grp + seq % RING_SLOTS);
+    return bars_local + 8u * (2u * RECV_BARS + (uint32_t)RING_SLOTS * (uint32_t)grp + seq % RING_SLOTS);
   }
   __device__ __forceinline__ void issue_next() {  // thread 0 of a combiner group only
     next_m = pair_next_active(abar, n, next_m);
@@ -135,7 +143,7 @@ struct DeviceEnv {
   }
   __device__ __forceinline__ void start(const uint16_t*, int) {
     if (tid == 0) {
-      for (int b = 0; b < 2 + 2 * RING_SLOTS; ++b)
+      for (int b = 0; b < 2 * RECV_BARS + 2 * RING_SLOTS; ++b)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars_local + 8u * b) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -181,19 +189,24 @@ struct DeviceEnv {
   __device__ __forceinline__ void keys_taken(uint32_t step) {
     asm volatile("bar.arrive %0, %1;" ::"r"(BAR_KEYS_EMPTY + 2 * grp + (int)(step & 1u)), "n"(PAIR_THREADS) : "memory");
   }
-  __device__ __forceinline__ void arm_recv(uint32_t step) {  // 4 KB from the peer's group 1
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bars_local + 8u * (step & 1u)), "r"(RECV_WORDS * 4)
-                 : "memory");
+  __device__ __forceinline__ void arm_recv(uint32_t step) {  // 4 KB from the peer's group 1, split over RECV_BARS barriers
+#pragma unroll
+    for (int j = 0; j < RECV_BARS; ++j)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bars_local + 8u * ((step & 1u) * RECV_BARS + j)),
+                   "r"(RECV_WORDS * 4 / RECV_BARS)
+                   : "memory");
   }
   __device__ __forceinline__ void send16(const uint32_t* v, uint32_t step) {
     const uint32_t buf = step & 1u;
     const uint32_t dst = recv_peer + (buf * RECV_WORDS + (uint32_t)t * 16u) * 4u;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) send4(dst + 16u * q, bars_peer + 8u * buf, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    for (int q = 0; q < 4; ++q)
+      send4(dst + 16u * q, bars_peer + 8u * (buf * RECV_BARS + q % RECV_BARS), v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   }
   __device__ __forceinline__ void recv16(uint32_t* r, uint32_t step) {
     const uint32_t buf = step & 1u;
-    wait_cluster_phase(bars_local + 8u * buf, (step >> 1) & 1u);
+#pragma unroll
+    for (int j = 0; j < RECV_BARS; ++j) wait_cluster_phase(bars_local + 8u * (buf * RECV_BARS + j), (step >> 1) & 1u);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       uint32_t a, b, c, d;
