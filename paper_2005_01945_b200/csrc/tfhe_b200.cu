@@ -153,11 +153,11 @@ __device__ __forceinline__ void bulk_load(void* dst_smem, const void* src_gmem, 
 #endif
 constexpr int K1D_WARPS = TFB_K1D_WARPS;
 #ifndef TFB_K1D_WAVE_TABLE  // ms per wave of K1d with 1 .. 12 gates per CTA (tools/k1_ab.py, TFB_K1D_W)
-#define TFB_K1D_WAVE_TABLE 3.33, 3.21, 3.24, 3.39, 4.85, 5.45, 5.53, 4.91, 6.64, 6.70, 6.82, 6.72
+#define TFB_K1D_WAVE_TABLE 3.25, 3.13, 3.20, 3.26, 4.74, 5.10, 5.15, 4.69, 6.64, 6.70, 6.82, 6.66
 #endif
 constexpr int K1D_THREADS = K1D_WARPS * WARP_T;
-__host__ __device__ constexpr int warp_smem(int n) {
-  return WBUF_BYTES + 2 * RING_N * (int)sizeof(uint32_t) + ((n + 2) * 2 + 15) / 16 * 16;
+__host__ __device__ constexpr int warp_smem(int n, bool split = true) {
+  return wbuf_bytes(split) + 2 * RING_N * (int)sizeof(uint32_t) + ((n + 2) * 2 + 15) / 16 * 16;
 }
 
 // Key ring of K1d: WR_SLOTS chunks of 12 KB (pair, stage, four spectral points per lane x three keys x two
@@ -279,7 +279,9 @@ struct WarpRing {
 #ifndef TFB_K1D_TURNS
 #define TFB_K1D_TURNS 0
 #endif
+template <bool SPLIT>
 struct DevWarp {
+  static constexpr bool kSplitExchange = SPLIT;  // two rounds through a half-size buffer (twelve warps per CTA) or one
   int turn_wait = 0, turn_next = 0;  // named-barrier ids (0: no protocol, e.g. the key-setup kernel)
 #ifdef TFB_K1D_PHASES
   mutable long long T[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, last = 0;
@@ -415,6 +417,7 @@ struct TmemTw {
   }
 };
 
+template <bool SPLIT>
 __device__ __forceinline__ void k1d_body(
     const uint32_t* __restrict__ pool, const uint8_t* __restrict__ kinds,
     const int32_t* __restrict__ x_rows, const int32_t* __restrict__ y_rows, int stride, int n, uint32_t mu,
@@ -426,9 +429,9 @@ __device__ __forceinline__ void k1d_body(
   cd* ring = reinterpret_cast<cd*>(smem + K1D_OFF_RING);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K1D_OFF_BARS);
   const int wid = threadIdx.x / WARP_T, t = threadIdx.x % WARP_T;
-  unsigned char* mine = smem + K1D_HEADER + (size_t)wid * warp_smem(n);
+  unsigned char* mine = smem + K1D_HEADER + (size_t)wid * warp_smem(n, SPLIT);
   void* buf = mine;
-  uint32_t* acc = reinterpret_cast<uint32_t*>(mine + WBUF_BYTES);
+  uint32_t* acc = reinterpret_cast<uint32_t*>(mine + wbuf_bytes(SPLIT));
   uint16_t* abar = reinterpret_cast<uint16_t*>(acc + 2 * RING_N);
 
   // warps of this CTA: K1D_WARPS in a throughput launch, fewer when a mid-size launch is spread over all SMs
@@ -479,7 +482,7 @@ __device__ __forceinline__ void k1d_body(
   const uint32_t* xr = pool + (int64_t)x_rows[g] * stride;
   const uint32_t* yr = pool + (int64_t)y_rows[g] * stride;
   uint32_t* dst = want < k ? ext + g * EXT_STRIDE : nullptr;  // null: no extract
-  DevWarp w;
+  DevWarp<SPLIT> w;
 #if TFB_K1D_TURNS
   {
     // rotation over the warps {s, s + 4, s + 8} of scheduler s = wid % 4 (grouping {3 s, 3 s + 1, 3 s + 2} measured
@@ -530,12 +533,16 @@ __device__ __forceinline__ void k1d_body(
       int64_t k
 // the throughput build: up to twelve warps per CTA, 168 registers per thread
 __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(TFB_K1D_ARGS) {
-  k1d_body(pool, kinds, x_rows, y_rows, stride, n, mu, bkw, tw_global, ft_global, ext, k);
+  k1d_body<true>(pool, kinds, x_rows, y_rows, stride, n, mu, bkw, tw_global, ft_global, ext, k);
 }
 // the same code for the mid-size launches that run at most eight warps per CTA: 255 registers per thread
 constexpr int K1D_WARPS_MID = 8;
+#ifndef TFB_K1D_MID_SPLIT
+#define TFB_K1D_MID_SPLIT 0  // eight warps leave room for full-size exchange buffers: one round instead of two
+#endif
+constexpr bool K1D_MID_SPLIT = TFB_K1D_MID_SPLIT != 0;
 __global__ void __launch_bounds__(K1D_WARPS_MID * WARP_T, 1) k_gate_bootstrap_warp_mid(TFB_K1D_ARGS) {
-  k1d_body(pool, kinds, x_rows, y_rows, stride, n, mu, bkw, tw_global, ft_global, ext, k);
+  k1d_body<K1D_MID_SPLIT>(pool, kinds, x_rows, y_rows, stride, n, mu, bkw, tw_global, ft_global, ext, k);
 }
 
 // ------------------------------------------------------------------------------------
@@ -737,7 +744,7 @@ __global__ void __launch_bounds__(WARP_T) k_bk_transform_w(const int32_t* __rest
 #pragma unroll
   for (int m = 0; m < WPTS; ++m)
     x[m] = cd{int32_to_double(src[t + 32 * m]), int32_to_double(src[t + 32 * m + HALF_N])};
-  DevWarp w;
+  DevWarp<WX_SPLIT> w;
   LaneTwiddles lt;
   build_lane_twiddles(tw, t, &lt);
   wfft_forward(x, t, MemTw{&lt}, buf, w);
@@ -956,7 +963,7 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
                              K1D_HEADER + K1D_WARPS * warp_smem(p->n));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gate_bootstrap_warp_mid, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             K1D_HEADER + K1D_WARPS_MID * warp_smem(p->n));
+                             K1D_HEADER + K1D_WARPS_MID * warp_smem(p->n, K1D_MID_SPLIT));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k1e::k_gate_bootstrap_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, k1e::smem_bytes(p->n));
   if (e == cudaSuccess)
@@ -1119,8 +1126,9 @@ static int launch_k1_variant(tfb_ctx* ctx, int which, int warps, const void* poo
                       ? ctx->force_warps
                       : (warps >= 1 && warps <= K1D_WARPS ? warps : K1D_WARPS);
     const unsigned grid = (unsigned)((k + w - 1) / w);
-    auto kernel = (w <= K1D_WARPS_MID && !ctx->force_wide_regs) ? k_gate_bootstrap_warp_mid : k_gate_bootstrap_warp;
-    kernel<<<grid, w * WARP_T, K1D_HEADER + w * warp_smem(n), st>>>(
+    const bool mid = w <= K1D_WARPS_MID && !ctx->force_wide_regs;
+    auto kernel = mid ? k_gate_bootstrap_warp_mid : k_gate_bootstrap_warp;
+    kernel<<<grid, w * WARP_T, K1D_HEADER + w * warp_smem(n, mid ? K1D_MID_SPLIT : true), st>>>(
         (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ctx->d_ft, ext, k);
   } else {
     ctx->err = "unknown K1 variant (4 = K1d warp kernel, 5 = K1e cluster kernel)";

@@ -212,7 +212,8 @@ TFB_HD int wspectral_index(int t, int q) { return (t & 15) + 16 * (2 * q + (t >>
 #define TFB_K1D_SPLIT 1
 #endif
 constexpr bool WX_SPLIT = TFB_K1D_SPLIT != 0;
-constexpr int WBUF_BYTES = WX_ROW * 16 * (WX_SPLIT ? 8 : 16);
+TFB_HD constexpr int wbuf_bytes(bool split) { return WX_ROW * 16 * (split ? 8 : 16); }
+constexpr int WBUF_BYTES = wbuf_bytes(WX_SPLIT);
 
 template <bool FWD>
 TFB_HD int wx_src(int t, int k) {  // slot of register k on the side that holds (r, h)-ordered data
@@ -220,9 +221,10 @@ TFB_HD int wx_src(int t, int k) {  // slot of register k on the side that holds 
 }
 TFB_HD int wx_dst(int t, int k) { return wslot(k, t & 15, t >> 4); }  // (k1, b)-ordered side, register k = r
 
+// (W::kSplitExchange: the warp environment says which; a CTA of at most eight warps has the room for one round)
 template <bool FWD, class W>
 TFB_HD void wexchange(cd* x, int t, void* buf, W& w) {
-  if (WX_SPLIT) {
+  if (W::kSplitExchange) {
     double* b = reinterpret_cast<double*>(buf);
 #pragma unroll
     for (int k = 0; k < WPTS; ++k) b[FWD ? wx_src<FWD>(t, k) : wx_dst(t, k)] = x[k].re;

@@ -209,6 +209,7 @@ void emu_ks_digits(const uint32_t* ext, int32_t* digits_out) {
 // ---- K1d: one ciphertext per warp (tfhe_warp.cuh), 32 host threads per warp ----------------
 namespace {
 struct EmuWarp {
+  static constexpr bool kSplitExchange = WX_SPLIT;
   pthread_barrier_t* b;
   cd* scratch;  // 32 cd
   int lane;
