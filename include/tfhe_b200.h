@@ -127,7 +127,7 @@ int tfb_debug_spectral_key(tfb_ctx *ctx, int32_t pair, int32_t key, double *out_
 /* K1 dispatch, host logic only (no GPU needed): the kernel launches a fused bootstrap of k gates is split
  * into on a device with `sms` multiprocessors.  Segment i covers gates[i] consecutive gates and runs as
  * variants[i] = 4 (K1d, one gate per warp, warps[i] = 1..12 gates per CTA: throughput) or 5 (K1e, one gate per
- * two-CTA cluster: latency; warps[i] = 0).  Returns the number of segments (at most 4); arrays may be NULL. */
+ * two-CTA cluster: latency; warps[i] = 0).  Returns the number of segments (at most 6); arrays may be NULL. */
 int tfb_debug_plan_kernels(int64_t k, int sms, int32_t *variants, int32_t *warps, int64_t *gates, int max_segments);
 
 /* Number of kernels this context has launched so far (bench `gpu_launches`). */

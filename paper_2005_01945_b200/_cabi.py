@@ -150,8 +150,8 @@ class Context:
 def plan_kernels(k: int, sms: int = 148) -> list[tuple[int, int, int]]:
     """The kernel launches a fused bootstrap of k gates runs as: [(variant, gates per CTA, gates)], variant
     4 = K1d (one gate per warp), 5 = K1e (one gate per two-CTA cluster; gates per CTA reported as 0)."""
-    v, w, g = (ctypes.c_int32 * 4)(), (ctypes.c_int32 * 4)(), (ctypes.c_int64 * 4)()
-    n = lib().tfb_debug_plan_kernels(int(k), int(sms), v, w, g, 4)
+    v, w, g = (ctypes.c_int32 * 8)(), (ctypes.c_int32 * 8)(), (ctypes.c_int64 * 8)()
+    n = lib().tfb_debug_plan_kernels(int(k), int(sms), v, w, g, 8)
     return [(int(v[i]), int(w[i]), int(g[i])) for i in range(n)]
 
 

@@ -1081,37 +1081,51 @@ static double k1_simple(int64_t k, int sms, K1Seg* seg) {
   *seg = t_e <= t_d ? K1Seg{5, 0, k} : K1Seg{4, w, k};
   return t_e <= t_d ? t_e : t_d;
 }
-// K1 dispatch.  K1e (one gate per two-SM cluster) wins on latency, K1d (one gate per warp) on throughput: full
-// waves of twelve gates per SM first; the ragged rest (or a launch below one wave) as the cheapest of: cluster
-// waves, one K1d wave of narrower CTAs on every SM, or a balanced K1d wave (4 or 8 gates per SM: one or two warps
-// on every scheduler) followed by one of the former.  Returns the number of segments.
+// K1 dispatch.  K1e (one gate per two-SM cluster) wins on latency, K1d (one gate per warp) on throughput.  A launch
+// is covered by waves of 12, 8 and 4 gates per SM (three, two, one warp on every scheduler: 6.66 / 4.69 / 3.26 ms for
+// 1776 / 1184 / 592 gates on 148 SMs) plus one tail -- the cheapest of cluster waves or one K1d wave of narrower CTAs
+// -- and the cheapest combination wins: mostly twelve-warp waves, but e.g. 4096 gates = 1776 + 2 x 1184 + a tail
+// instead of 2 x 1776 + a poorly filled third wave.  Returns the number of segments (one kernel launch each).
+constexpr int K1_MAX_SEGS = 6;
 static int plan_k1(int64_t k, int sms, K1Seg* seg) {
-  int nseg = 0;
-  const int64_t wave_d = (int64_t)sms * K1D_WARPS;
-  const int64_t full = k / wave_d * wave_d, rest = k - full;
-  if (full) seg[nseg++] = K1Seg{4, K1D_WARPS, full};
-  if (rest == 0) return nseg;
-  K1Seg one, head, tail;
-  double best = k1_simple(rest, sms, &one);
-  int two = 0;
-  for (int w = 4; w <= 8; w += 4) {
-    const int64_t part = (int64_t)w * sms;
-    if (rest <= part) break;
-    K1Seg t;
-    const double c = K1D_WAVE_MS[w] + k1_simple(rest - part, sms, &t);
-    if (c < best) {
-      best = c;
-      two = 1;
-      head = K1Seg{4, w, part};
-      tail = t;
+  const int64_t cap12 = (int64_t)sms * K1D_WARPS, cap8 = (int64_t)sms * 8, cap4 = (int64_t)sms * 4;
+  const int64_t max12 = k / cap12;
+  double best = 1e300;
+  int64_t best12 = 0, best8 = 0, best4 = 0;
+  K1Seg best_tail{0, 0, 0};
+  for (int64_t n12 = max12 > 0 ? max12 - 1 : 0; n12 <= max12; ++n12) {
+    const int64_t r12 = k - n12 * cap12;
+    for (int64_t n8 = 0; n8 <= 3 && n8 * cap8 <= r12; ++n8) {
+      const int64_t r8 = r12 - n8 * cap8;
+      for (int64_t n4 = 0; n4 <= 1 && n4 * cap4 <= r8; ++n4) {
+        const int64_t r4 = r8 - n4 * cap4;
+        if (r4 > cap12) continue;  // the tail is at most one wave of the widest CTAs
+        K1Seg tail{0, 0, 0};
+        const double c = (double)n12 * K1D_WAVE_MS[K1D_WARPS] + (double)n8 * K1D_WAVE_MS[8] + (double)n4 * K1D_WAVE_MS[4] +
+                         (r4 ? k1_simple(r4, sms, &tail) : 0.0);
+        if (c < best - 1e-9) {
+          best = c;
+          best12 = n12, best8 = n8, best4 = n4;
+          best_tail = tail;
+        }
+      }
     }
   }
-  if (two) {
-    seg[nseg++] = head;
-    seg[nseg++] = tail;
-  } else {
-    seg[nseg++] = one;
-  }
+  int nseg = 0;
+  auto push = [&](K1Seg sg) {
+    if (!sg.gates) return;
+    if (nseg && seg[nseg - 1].which == sg.which && seg[nseg - 1].warps == sg.warps)
+      seg[nseg - 1].gates += sg.gates;  // same kernel, same CTA width: one launch
+    else
+      seg[nseg++] = sg;
+  };
+  const bool tail12 = best_tail.which == 4 && best_tail.warps == K1D_WARPS;  // rides in the twelve-warp launch
+  push(K1Seg{4, K1D_WARPS, best12 * cap12});
+  if (tail12) push(best_tail);
+  push(K1Seg{4, 8, best8 * cap8});
+  if (best_tail.which == 4 && best_tail.warps == 8) push(best_tail);
+  push(K1Seg{4, 4, best4 * cap4});
+  if (!tail12 && !(best_tail.which == 4 && best_tail.warps == 8)) push(best_tail);
   return nseg;
 }
 
@@ -1143,7 +1157,7 @@ static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, int stride, const
                                const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
   if (ctx->force_kernel)
     return launch_k1_variant(ctx, ctx->force_kernel, 0, pool, stride, kinds, xr, yr, ext, k, st);
-  K1Seg seg[4];
+  K1Seg seg[K1_MAX_SEGS];
   const int nseg = plan_k1(k, ctx->sm_count, seg);
   int64_t at = 0;
   for (int i = 0; i < nseg; ++i) {
@@ -1356,7 +1370,7 @@ int tfb_debug_spectral_key(tfb_ctx* ctx, int32_t pair, int32_t key, double* out)
 
 int tfb_debug_plan_kernels(int64_t k, int sms, int32_t* variants, int32_t* warps, int64_t* gates, int max_segments) {
   if (k < 1 || sms < 1) return 0;
-  K1Seg seg[4];
+  K1Seg seg[K1_MAX_SEGS];
   const int nseg = plan_k1(k, sms, seg);
   for (int i = 0; i < nseg && i < max_segments; ++i) {
     if (variants) variants[i] = seg[i].which;

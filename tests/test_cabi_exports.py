@@ -62,16 +62,17 @@ def test_k1_dispatch_plan(library):
     assert plan(148) == [(5, 0, 148)]                       # two cluster waves beat one warp-kernel wave
     assert plan(592) == [(4, 4, 592)]                       # one warp on every scheduler of every SM
     assert plan(1184) == [(4, 8, 1184)] and plan(1776) == [(4, 12, 1776)] and plan(3552) == [(4, 12, 3552)]
-    segs = plan(1 << 16)                                    # BASELINE configs[1]: 36 full waves, then the rest
-    assert segs[0] == (4, 12, 36 * 1776) and sum(g for _, _, g in segs) == 1 << 16
+    assert plan(1 << 16) == [(4, 12, 1 << 16)]              # BASELINE configs[1]: 36 full waves + a last one, one launch
     assert plan(2 * 1776 + 30) == [(4, 12, 2 * 1776), (5, 0, 30)]  # ragged: a short tail on the clusters
-    for k in (1, 7, 149, 297, 600, 700, 1000, 1777, 2500, 5000, 100000):
+    assert plan(4096) == [(4, 12, 1776), (4, 8, 2320)]      # two eight-warp waves beat a poorly filled third wave
+    assert plan(2500) == [(4, 8, 2368), (5, 0, 132)]
+    for k in (1, 7, 149, 297, 600, 700, 1000, 1777, 2500, 5000, 8192, 100000):
         segs = plan(k)
-        assert 1 <= len(segs) <= 4 and sum(g for _, _, g in segs) == k
+        assert 1 <= len(segs) <= 6 and sum(g for _, _, g in segs) == k
         for which, warps, gates in segs:
             assert gates > 0 and ((which == 5 and warps == 0) or (which == 4 and 1 <= warps <= 12))
-            if which == 4:
-                assert gates <= 148 * warps or warps == 12  # a narrower wave fits the chip once
+            if which == 4 and warps not in (4, 8, 12):
+                assert gates <= 148 * warps                 # an odd CTA width is a single wave
     assert plan(1776 // 2, sms=74) == [(4, 12, 888)]        # scales with the SM count
 
 

@@ -266,7 +266,7 @@ def test_automatic_dispatch_sizes(gpu, key, eval_keys):
     base = 64
     xs, ys, kinds, bits = make_inputs(key, base, seed=37)
     want = orc.gate_bootstrap_batch(xs, ys, kinds, key.params.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
-    for K in (1, 2, 33, 297, 400, 889, 1030, 1775, 1777, 1800, 2500):
+    for K in (1, 2, 33, 297, 400, 889, 1030, 1775, 1777, 1800, 2500, 4096):
         idx = np.arange(K) % base
         got = run_launch(gpu, key, xs[idx], ys[idx], kinds[idx])
         assert np.array_equal(got, want[idx]), K
