@@ -15,6 +15,11 @@
  * asynchronous but is not required); `stream` is a cudaStream_t passed as
  * void* (NULL = the legacy default stream).  Nothing throws across the ABI.
  *
+ * Threading: like the reference's engine (single driver thread, encirc/scheduler.py:173-179) a context is driven
+ * by one thread at a time, and its gate launches must be ordered on ONE stream at a time: the scratch between the
+ * fused bootstrap and the key switch (extracted samples, the partial sums of narrow launches) belongs to the context.
+ * Use one context per stream / per device for concurrent work.
+ *
  * Ciphertext layout: one LWE sample is n mask words followed by one body word
  * (uint32, torus 2^-32 fixed point; encirc/torus.py:190-203).  In the device
  * pool a sample occupies one row of TFB_ROW_STRIDE words (the tail is padding);
