@@ -64,9 +64,12 @@ def _comm_device(engine):
     import torch
 
     dist = _dist()
-    if dist.is_initialized() and dist.get_backend() == "nccl":
-        return getattr(engine, "device", torch.device("cuda"))
-    return torch.device("cpu")
+    if dist.is_initialized():
+        if dist.get_backend() == "nccl":
+            return getattr(engine, "device", torch.device("cuda"))
+        return torch.device("cpu")
+    # a single process without a process group: nothing is communicated, the words stay where the engine keeps them
+    return getattr(engine, "device", torch.device("cpu"))
 
 
 def _as_tensor(words, device):
