@@ -18,6 +18,7 @@
 //                         (tcgen05.mma kind::i8, TMEM accumulator), tfhe_keyswitch_mma.cuh
 //   K3 k_bk_transform(_w) one-time: raw TRGSW rows -> spectral key in K1e's / K1d's chunk order;
 //      k_ksk_layout       raw key-switching key -> row-padded table
+//   k_partition_trivial, k_trivial_extract   regrouping of a launch: gates on two trivial inputs behind the real ones
 //   k_rows_negate, k_rows_phase, k_rows_encrypt   NOT, batched phase (decryption helper), batched encryption
 //   k_peak_*              DFMA / IMAD peak microbenchmarks (roofline denominators)
 #include <cuda_runtime.h>
@@ -59,6 +60,8 @@ struct tfb_ctx {
   uint32_t* d_ext = nullptr;   // scratch [cap][EXT_STRIDE]
   uint32_t* d_ksn = nullptr;   // K2n partial sums + counters (KSN_SCRATCH_WORDS, zero between launches)
   int64_t ext_cap = 0;
+  int32_t* d_perm = nullptr;   // regrouped launch: [3][cap] x / y / out rows, then [cap] kinds (bytes), then 2 counters
+  int no_regroup = 0;          // 1: launches keep the caller's gate order (profiling)
   // buffers of the host-buffer launch path
   uint32_t* d_hx = nullptr;    // [cap][ROW_STRIDE] x, y, out back to back
   uint8_t* d_hkinds = nullptr;
@@ -530,9 +533,15 @@ __device__ __forceinline__ void k1d_body(
   const uint32_t *__restrict__ pool, const uint8_t *__restrict__ kinds, const int32_t *__restrict__ x_rows,           \
       const int32_t *__restrict__ y_rows, int stride, int n, uint32_t mu, const cd *__restrict__ bkw,                 \
       const WarpTwiddles *__restrict__ tw_global, const FactorTables *__restrict__ ft_global, uint32_t *__restrict__ ext, \
-      int64_t k
+      int64_t k, const uint32_t *__restrict__ active, int64_t gate0
 // the throughput build: up to twelve warps per CTA, 168 registers per thread
+// `active` (may be null): a regrouped launch keeps its gates with two trivial inputs behind the first *active ones
+// (k_partition_trivial); their extracted samples are written by k_trivial_extract, and a CTA that holds only such
+// gates has nothing to do.
+#define TFB_K1D_SKIP_IDLE_CTA \
+  if (active && gate0 + (int64_t)blockIdx.x * (int64_t)(blockDim.x / WARP_T) >= (int64_t)*active) return;
 __global__ void __launch_bounds__(K1D_THREADS, 1) k_gate_bootstrap_warp(TFB_K1D_ARGS) {
+  TFB_K1D_SKIP_IDLE_CTA
   k1d_body<true>(pool, kinds, x_rows, y_rows, stride, n, mu, bkw, tw_global, ft_global, ext, k);
 }
 // the same code for the mid-size launches that run at most eight warps per CTA: 255 registers per thread
@@ -542,6 +551,7 @@ constexpr int K1D_WARPS_MID = 8;
 #endif
 constexpr bool K1D_MID_SPLIT = TFB_K1D_MID_SPLIT != 0;
 __global__ void __launch_bounds__(K1D_WARPS_MID * WARP_T, 1) k_gate_bootstrap_warp_mid(TFB_K1D_ARGS) {
+  TFB_K1D_SKIP_IDLE_CTA
   k1d_body<K1D_MID_SPLIT>(pool, kinds, x_rows, y_rows, stride, n, mu, bkw, tw_global, ft_global, ext, k);
 }
 
@@ -691,6 +701,67 @@ __global__ void __launch_bounds__(KS_THREADS) k_key_switch_narrow(const uint32_t
     }
   }
   if (tid == 0) *counter = 0u;
+}
+
+// Regrouping of a launch: gates whose two inputs are trivial (zero masks: the zero padding of multiplier trees,
+// constants) have nothing to rotate -- their accumulator stays the rotated test vector -- but inside a K1d CTA they
+// hold warps that run at the pace of the busy ones.  k_partition_trivial moves them behind the real gates (one warp
+// per gate reads the two masks; a CTA claims its output ranges with two atomics; the order inside a group is
+// arbitrary: gates of a launch are independent and every gate carries its own rows), k_trivial_extract writes their
+// extracted samples, and K1 CTAs that hold only such gates return at once (`active`).
+constexpr int PART_GATES_PER_CTA = 32;
+__global__ void __launch_bounds__(256) k_partition_trivial(const uint32_t* __restrict__ pool, int stride, int n,
+                                                          const uint8_t* __restrict__ kinds, const int32_t* __restrict__ xr,
+                                                          const int32_t* __restrict__ yr, const int32_t* __restrict__ orow,
+                                                          int64_t k, int32_t* __restrict__ perm, uint32_t* __restrict__ counters) {
+  __shared__ uint8_t idle[PART_GATES_PER_CTA];
+  __shared__ int32_t slot[PART_GATES_PER_CTA];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t g0 = (int64_t)blockIdx.x * PART_GATES_PER_CTA;
+  for (int j = warp; j < PART_GATES_PER_CTA; j += 8) {
+    const int64_t g = g0 + j;
+    uint32_t any = 0;
+    if (g < k) {
+      const uint32_t* x = pool + (int64_t)xr[g] * stride;
+      const uint32_t* y = pool + (int64_t)yr[g] * stride;
+      for (int i = lane; i < n; i += 32) any |= x[i] | y[i];
+    }
+    any = __reduce_or_sync(0xffffffffu, any);
+    if (lane == 0) idle[j] = (g < k && any == 0) ? 1 : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int live = (int)min((int64_t)PART_GATES_PER_CTA, k - g0);
+    int n_idle = 0;
+    for (int j = 0; j < live; ++j) n_idle += idle[j];
+    const uint32_t front = atomicAdd(&counters[0], (uint32_t)(live - n_idle));  // real gates fill from the front ...
+    const uint32_t back = atomicAdd(&counters[1], (uint32_t)n_idle);             // ... trivial-input gates from the back
+    uint32_t f = front, b = back;
+    for (int j = 0; j < live; ++j) slot[j] = idle[j] ? (int32_t)(k - 1 - b++) : (int32_t)f++;
+  }
+  __syncthreads();
+  if (threadIdx.x < PART_GATES_PER_CTA && g0 + threadIdx.x < k) {
+    const int64_t g = g0 + threadIdx.x, s = slot[threadIdx.x];
+    perm[s] = xr[g];
+    perm[k + s] = yr[g];
+    perm[2 * k + s] = orow[g];
+    reinterpret_cast<uint8_t*>(perm + 3 * k)[s] = kinds[g];
+  }
+}
+// extracted sample of a gate on two trivial inputs: mask 0, body = coefficient 0 of the rotated test vector
+__global__ void __launch_bounds__(256) k_trivial_extract(const uint32_t* __restrict__ pool, int stride, int n, uint32_t mu,
+                                                        const uint8_t* __restrict__ kinds, const int32_t* __restrict__ xr,
+                                                        const int32_t* __restrict__ yr, uint32_t* __restrict__ ext, int64_t k,
+                                                        const uint32_t* __restrict__ active) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t g = (int64_t)*active + (int64_t)blockIdx.x * 8 + warp;  // one warp per gate behind the real ones
+  if (g >= k) return;
+  uint32_t* row = ext + g * EXT_STRIDE;
+  for (int j = lane; j < RING_N; j += 32) row[j] = 0u;
+  if (lane == 0) {
+    const int bbar = gate_body_rotation_of(pool + (int64_t)xr[g] * stride, pool + (int64_t)yr[g] * stride, (int)kinds[g], n, mu);
+    row[RING_N] = test_vector_coeff(0, bbar, mu);
+  }
 }
 
 __global__ void k_rows_zero(uint32_t* __restrict__ pool, const int32_t* __restrict__ rows, int stride, int n) {
@@ -910,6 +981,9 @@ static int ensure_ext(tfb_ctx* ctx, int64_t k) {
   int64_t cap = 1024;
   while (cap < k) cap *= 2;
   TFB_CUDA(ctx, cudaMalloc(&ctx->d_ext, (size_t)cap * EXT_STRIDE * sizeof(uint32_t)));
+  if (ctx->d_perm) TFB_CUDA(ctx, cudaFree(ctx->d_perm));
+  ctx->d_perm = nullptr;
+  TFB_CUDA(ctx, cudaMalloc(&ctx->d_perm, (size_t)cap * 13 + 64));  // 3 x int32 + 1 byte per gate, two counters
   ctx->ext_cap = cap;
   return TFB_OK;
 }
@@ -982,6 +1056,7 @@ int tfb_ctx_create(int device, const tfb_params* p, tfb_ctx** out) {
   if (const char* f = getenv("TFB_K1D_W")) ctx->force_warps = atoi(f);
   if (const char* f = getenv("TFB_K1D_NOMID")) ctx->force_wide_regs = atoi(f);
   if (const char* f = getenv("TFB_FORCE_KS")) ctx->force_ks = atoi(f);
+  if (const char* f = getenv("TFB_NO_REGROUP")) ctx->no_regroup = atoi(f);
   *out = ctx;
   return TFB_OK;
 }
@@ -998,6 +1073,7 @@ void tfb_ctx_destroy(tfb_ctx* ctx) {
   cudaFree(ctx->d_tw);
   cudaFree(ctx->d_ext);
   cudaFree(ctx->d_ksn);
+  cudaFree(ctx->d_perm);
   cudaFree(ctx->d_hx);
   cudaFree(ctx->d_hkinds);
   cudaFree(ctx->d_hrows);
@@ -1130,7 +1206,8 @@ static int plan_k1(int64_t k, int sms, K1Seg* seg) {
 }
 
 static int launch_k1_variant(tfb_ctx* ctx, int which, int warps, const void* pool, int stride, const uint8_t* kinds,
-                             const int32_t* xr, const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
+                             const int32_t* xr, const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st,
+                             const uint32_t* active = nullptr, int64_t gate0 = 0) {
   const int n = ctx->p.n;
   if (which == 5) {  // one gate per two-CTA cluster (the kernel carries __cluster_dims__(2, 1, 1))
     k1e::k_gate_bootstrap_pair<<<(unsigned)(2 * k), k1e::THREADS, k1e::smem_bytes(n), st>>>(
@@ -1143,7 +1220,7 @@ static int launch_k1_variant(tfb_ctx* ctx, int which, int warps, const void* poo
     const bool mid = w <= K1D_WARPS_MID && !ctx->force_wide_regs;
     auto kernel = mid ? k_gate_bootstrap_warp_mid : k_gate_bootstrap_warp;
     kernel<<<grid, w * WARP_T, K1D_HEADER + w * warp_smem(n, mid ? K1D_MID_SPLIT : true), st>>>(
-        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ctx->d_ft, ext, k);
+        (const uint32_t*)pool, kinds, xr, yr, stride, n, ctx->p.mu_word, ctx->d_bkw, ctx->d_wtw, ctx->d_ft, ext, k, active, gate0);
   } else {
     ctx->err = "unknown K1 variant (4 = K1d warp kernel, 5 = K1e cluster kernel)";
     return TFB_ERR_INVALID;
@@ -1154,7 +1231,8 @@ static int launch_k1_variant(tfb_ctx* ctx, int which, int warps, const void* poo
 }
 
 static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, int stride, const uint8_t* kinds, const int32_t* xr,
-                               const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st) {
+                               const int32_t* yr, uint32_t* ext, int64_t k, cudaStream_t st,
+                               const uint32_t* active = nullptr) {
   if (ctx->force_kernel)
     return launch_k1_variant(ctx, ctx->force_kernel, 0, pool, stride, kinds, xr, yr, ext, k, st);
   K1Seg seg[K1_MAX_SEGS];
@@ -1162,7 +1240,7 @@ static int launch_blind_rotate(tfb_ctx* ctx, const void* pool, int stride, const
   int64_t at = 0;
   for (int i = 0; i < nseg; ++i) {
     int rc = launch_k1_variant(ctx, seg[i].which, seg[i].warps, pool, stride, kinds + at, xr + at, yr + at,
-                               ext + at * EXT_STRIDE, seg[i].gates, st);
+                               ext + at * EXT_STRIDE, seg[i].gates, st, active, at);
     if (rc) return rc;
     at += seg[i].gates;
   }
@@ -1226,7 +1304,23 @@ int tfb_gate_launch(tfb_ctx* ctx, void* pool, const uint8_t* kinds, const int32_
   cudaStream_t st = (cudaStream_t)stream;
   TFB_ENTER(ctx);
   if ((rc = ensure_ext(ctx, k))) return rc;
-  if ((rc = launch_blind_rotate(ctx, pool, ROW_STRIDE, kinds, xr, yr, ctx->d_ext, k, st))) return rc;
+  const uint32_t* active = nullptr;
+  if (k >= 4 * (int64_t)ctx->sm_count && !ctx->no_regroup && !ctx->force_kernel) {  // launches that run K1d: regroup
+    int32_t* perm = ctx->d_perm;
+    uint32_t* counters = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(perm) + (((size_t)k * 13 + 15) / 16) * 16);
+    TFB_CUDA(ctx, cudaMemsetAsync(counters, 0, 8, st));
+    k_partition_trivial<<<(unsigned)((k + PART_GATES_PER_CTA - 1) / PART_GATES_PER_CTA), 256, 0, st>>>(
+        (const uint32_t*)pool, ROW_STRIDE, ctx->p.n, kinds, xr, yr, out_rows, k, perm, counters);
+    kinds = reinterpret_cast<const uint8_t*>(perm + 3 * k);
+    xr = perm, yr = perm + k, out_rows = perm + 2 * k;
+    active = counters;
+    // (grid sized for k trivial gates; CTAs past the end return at once)
+    k_trivial_extract<<<(unsigned)((k + 7) / 8), 256, 0, st>>>((const uint32_t*)pool, ROW_STRIDE, ctx->p.n, ctx->p.mu_word, kinds, xr, yr,
+                                                  ctx->d_ext, k, active);
+    ctx->launches += 2;
+    TFB_CUDA(ctx, cudaGetLastError());
+  }
+  if ((rc = launch_blind_rotate(ctx, pool, ROW_STRIDE, kinds, xr, yr, ctx->d_ext, k, st, active))) return rc;
   return launch_key_switch(ctx, ctx->d_ext, pool, ROW_STRIDE, out_rows, k, st);
 }
 

@@ -342,6 +342,12 @@ TFB_HD void pair_rotations(const uint16_t* sm_abar, int n, int m, int& a1, int& 
   a1 = sm_abar[2 * m];
   a2 = (2 * m + 1 < n) ? sm_abar[2 * m + 1] : 0;
 }
+// the body's rotation alone (what a gate on two trivial inputs needs: its mask rotations are all zero)
+TFB_HD int gate_body_rotation_of(const uint32_t* x_row, const uint32_t* y_row, int kind, int n, uint32_t mu) {
+  int32_t cx, cy, off;
+  gate_coeffs(kind, cx, cy, off);
+  return mod_switch((uint32_t)cx * x_row[n] + (uint32_t)cy * y_row[n] + (uint32_t)off * mu);
+}
 // coefficient j of X^{2N - bbar} * mu (1 + X + ... + X^{N-1})
 TFB_HD uint32_t test_vector_coeff(int j, int bbar, uint32_t mu) {
   const int src = (j + bbar) & (2 * RING_N - 1);  // j - (2N - bbar) mod 2N

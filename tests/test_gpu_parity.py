@@ -175,6 +175,57 @@ def test_planned_segments_are_bit_exact(gpu, key, eval_keys):
     assert np.array_equal(got, want0[idx]), segs
 
 
+def test_regrouped_launch_with_trivial_inputs(key, eval_keys, monkeypatch):
+    """Launches of 4 x SMs gates and more are regrouped on the device: gates whose two inputs are trivial (zero
+    masks) go behind the real ones, their extracted samples are written directly and K1d CTAs that hold only such
+    gates return at once.  A third of the gates trivial, interleaved, scattered output rows, one gate writing over
+    its own input row: every output word equals the oracle's and the launch with regrouping switched off."""
+    import torch
+
+    from paper_2005_01945_b200 import _cabi
+
+    p, n = key.params, key.params.m
+    xs0, ys0, kinds0, _ = make_inputs(key, 10, seed=39, kinds=(np.arange(10) % 9).astype(np.uint8))
+    triv = np.zeros((2, n + 1), np.uint32)
+    triv[0, -1], triv[1, -1] = p.message_word(0), p.message_word(1)
+    base_x = np.concatenate([xs0, triv[[0, 1, 0, 1, 1, 0]]])
+    base_y = np.concatenate([ys0, triv[[0, 0, 1, 1, 0, 1]]])
+    base_k = np.concatenate([kinds0, np.array([0, 1, 2, 4, 7, 8], np.uint8)])
+    want = orc.gate_bootstrap_batch(base_x, base_y, base_k, p.mu.word, eval_keys.bk, eval_keys.ksk, fft=True)
+    dev = torch.device("cuda:0")
+    for K in (1000, 2100):
+        sel = np.where(np.arange(K) % 3 == 1, 10 + np.arange(K) % 6, np.arange(K) % 10)
+        outs = {}
+        for no_regroup in ("1", "0"):
+            monkeypatch.setenv("TFB_NO_REGROUP", no_regroup)
+            ctx = _cabi.Context(0, n, p.mu.word, eval_keys.ring)
+            ctx.call("tfb_load_keys", eval_keys.bk.ctypes.data, eval_keys.ksk.ctypes.data, 0, None)
+            pool = torch.zeros((3 * K, _cabi.ROW_STRIDE), dtype=torch.int32, device=dev)
+            pool[:K, : n + 1] = torch.from_numpy(base_x[sel].view(np.int32)).to(dev)
+            pool[K : 2 * K, : n + 1] = torch.from_numpy(base_y[sel].view(np.int32)).to(dev)
+            kd = torch.from_numpy(base_k[sel]).to(dev)
+            xr = torch.arange(0, K, dtype=torch.int32, device=dev)
+            yr = torch.arange(K, 2 * K, dtype=torch.int32, device=dev)
+            orow = (3 * K - 1 - torch.arange(0, K, dtype=torch.int32, device=dev)).contiguous()  # scattered, reversed
+            orow[5] = 5  # gate 5 overwrites its own x row
+            ctx.call("tfb_gate_launch", pool.data_ptr(), kd.data_ptr(), xr.data_ptr(), yr.data_ptr(), orow.data_ptr(), K, None)
+            torch.cuda.synchronize()
+            first = pool[orow.long(), : n + 1].cpu().numpy().view(np.uint32)
+            # again into fresh rows (the regrouping scratch is reused); row 5 now holds an output, so skip gate 5
+            orow2 = (torch.arange(0, K, dtype=torch.int32, device=dev) + 2 * K).contiguous()
+            ctx.call("tfb_gate_launch", pool.data_ptr(), kd.data_ptr(), xr.data_ptr(), yr.data_ptr(), orow2.data_ptr(), K, None)
+            torch.cuda.synchronize()
+            second = pool[orow2.long(), : n + 1].cpu().numpy().view(np.uint32)
+            outs[no_regroup] = (first, second)
+            ctx.close()
+        ok_rows = np.arange(K) != 5
+        assert np.array_equal(outs["1"][0], want[sel]), K
+        assert np.array_equal(outs["0"][0], outs["1"][0]), K
+        assert np.array_equal(outs["0"][1][ok_rows], want[sel][ok_rows]), K
+        idle = sel >= 10
+        assert not outs["0"][0][idle, :-1].any()  # two trivial inputs give a trivial output
+
+
 def test_key_switch_on_tensor_cores_is_exact(key, eval_keys, monkeypatch):
     """K2t (tcgen05.mma kind::i8: digits x byte planes of the key, s32 accumulators in tensor memory)
     against K2 (IMAD pipe) on arbitrary extracted samples, whole and partial 128-gate tiles, and against
