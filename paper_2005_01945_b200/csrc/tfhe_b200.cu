@@ -638,44 +638,51 @@ __global__ void __launch_bounds__(KS_THREADS) k_key_switch(const uint32_t* __res
 // group's counter reads the sums back, writes  (0, b) - sum  into the pool rows and clears scratch and counter
 // again (no separate zeroing kernel, nothing to order against the inputs).
 constexpr int KSN_G = 8;                     // gates per CTA
-constexpr int KSN_I = 4;                     // ring coefficients per CTA
-constexpr int KSN_ROWS = KSN_I * KS_T;       // 32 key rows
-constexpr int KSN_MAX_GATES = 32;            // launches up to this many gates take K2n
+constexpr int KSN_I = 4;                     // ring coefficients per batch of key loads
+constexpr int KSN_ROWS = KSN_I * KS_T;       // 32 key rows in flight per thread and batch
+constexpr int KSN_MAX_GATES = 96;            // launches below this many gates take K2n
+constexpr int KSN_SMALL_GATES = 16;          // up to here one batch per CTA (256 CTAs per group of 8 gates: shortest latency);
+constexpr int KSN_BATCHES_WIDE = 4;          // beyond, four batches per CTA (64 CTAs per group: a quarter of the atomics)
 constexpr int KSN_SCRATCH_WORDS = KSN_MAX_GATES * ROW_STRIDE + 64;  // sums, then one counter per gate group
+template <int BATCHES>
 __global__ void __launch_bounds__(KS_THREADS) k_key_switch_narrow(const uint32_t* __restrict__ ext,
                                                                   const int32_t* __restrict__ ksk,
                                                                   uint32_t* __restrict__ pool,
                                                                   const int32_t* __restrict__ out_rows, int stride, int n,
                                                                   int k, uint32_t* __restrict__ scratch) {
-  __shared__ int32_t digits[KSN_ROWS][KSN_G];
+  __shared__ int32_t digits[BATCHES][KSN_ROWS][KSN_G];
   __shared__ uint32_t arrived;
-  const int tid = threadIdx.x, i0 = blockIdx.x * KSN_I, g0 = blockIdx.y * KSN_G;
+  const int tid = threadIdx.x, i0 = blockIdx.x * KSN_I * BATCHES, g0 = blockIdx.y * KSN_G;
   const int live = min(KSN_G, k - g0);
-  // all key words of this thread first: 32 rows x 2 columns in flight
-  int32_t kw0[KSN_ROWS], kw1[KSN_ROWS];
-  const int32_t* kr = ksk + (int64_t)i0 * KS_T * ROW_STRIDE;
-#pragma unroll
-  for (int r = 0; r < KSN_ROWS; ++r) {
-    kw0[r] = __ldg(kr + r * ROW_STRIDE + tid);
-    kw1[r] = __ldg(kr + r * ROW_STRIDE + tid + KS_THREADS);
-  }
-  if (tid < KSN_I * KSN_G) {
-    const int c = tid / KSN_I, ii = tid % KSN_I;
-    const uint32_t ab = (c < live ? ext[(int64_t)(g0 + c) * EXT_STRIDE + i0 + ii] : 0u) + ks_bias();
-#pragma unroll
-    for (int j = 0; j < KS_T; ++j) digits[ii * KS_T + j][c] = c < live ? ks_digit(ab, j) : 0;
-  }
-  __syncthreads();
   int32_t acc0[KSN_G], acc1[KSN_G];
 #pragma unroll
   for (int c = 0; c < KSN_G; ++c) acc0[c] = acc1[c] = 0;
+#pragma unroll 1
+  for (int bt = 0; bt < BATCHES; ++bt) {
+    // all key words of the batch first: 32 rows x 2 columns in flight per thread ...
+    int32_t kw0[KSN_ROWS], kw1[KSN_ROWS];
+    const int32_t* kr = ksk + (int64_t)(i0 + bt * KSN_I) * KS_T * ROW_STRIDE;
 #pragma unroll
-  for (int r = 0; r < KSN_ROWS; ++r) {
+    for (int r = 0; r < KSN_ROWS; ++r) {
+      kw0[r] = __ldg(kr + r * ROW_STRIDE + tid);
+      kw1[r] = __ldg(kr + r * ROW_STRIDE + tid + KS_THREADS);
+    }
+    // ... then the batch's digits (its own shared-memory block: no barrier between batches)
+    if (tid < KSN_I * KSN_G) {
+      const int c = tid / KSN_I, ii = tid % KSN_I;
+      const uint32_t ab = (c < live ? ext[(int64_t)(g0 + c) * EXT_STRIDE + i0 + bt * KSN_I + ii] : 0u) + ks_bias();
 #pragma unroll
-    for (int c = 0; c < KSN_G; ++c) {
-      const int32_t d = digits[r][c];
-      acc0[c] += d * kw0[r];
-      acc1[c] += d * kw1[r];
+      for (int j = 0; j < KS_T; ++j) digits[bt][ii * KS_T + j][c] = c < live ? ks_digit(ab, j) : 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < KSN_ROWS; ++r) {
+#pragma unroll
+      for (int c = 0; c < KSN_G; ++c) {
+        const int32_t d = digits[bt][r][c];
+        acc0[c] += d * kw0[r];
+        acc1[c] += d * kw1[r];
+      }
     }
   }
   uint32_t* sums = scratch + (int64_t)g0 * ROW_STRIDE;
@@ -1261,9 +1268,14 @@ static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, int 
     TFB_CUDA(ctx, cudaGetLastError());
     return TFB_OK;
   }
-  if (k <= KSN_MAX_GATES && (ctx->force_ks == 0 || ctx->force_ks == 3)) {
-    k_key_switch_narrow<<<dim3(RING_N / KSN_I, (unsigned)((k + KSN_G - 1) / KSN_G)), KS_THREADS, 0, st>>>(
-        ext, ctx->d_ksk, (uint32_t*)pool, out_rows, stride, ctx->p.n, (int)k, ctx->d_ksn);
+  if (k < KSN_MAX_GATES && (ctx->force_ks == 0 || ctx->force_ks == 3)) {
+    const unsigned groups = (unsigned)((k + KSN_G - 1) / KSN_G);
+    if (k <= KSN_SMALL_GATES)
+      k_key_switch_narrow<1><<<dim3(RING_N / KSN_I, groups), KS_THREADS, 0, st>>>(
+          ext, ctx->d_ksk, (uint32_t*)pool, out_rows, stride, ctx->p.n, (int)k, ctx->d_ksn);
+    else
+      k_key_switch_narrow<KSN_BATCHES_WIDE><<<dim3(RING_N / (KSN_I * KSN_BATCHES_WIDE), groups), KS_THREADS, 0, st>>>(
+          ext, ctx->d_ksk, (uint32_t*)pool, out_rows, stride, ctx->p.n, (int)k, ctx->d_ksn);
     ctx->launches += 1;
     TFB_CUDA(ctx, cudaGetLastError());
     return TFB_OK;

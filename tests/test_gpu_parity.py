@@ -269,7 +269,7 @@ def test_key_switch_on_tensor_cores_is_exact(key, eval_keys, monkeypatch):
     monkeypatch.setenv("TFB_FORCE_KS", "3")
     ctxs["3"] = _cabi.Context(0, n, key.params.mu.word, eval_keys.ring)
     ctxs["3"].call("tfb_load_keys", eval_keys.bk.ctypes.data, eval_keys.ksk.ctypes.data, 0, None)
-    for K in (1, 2, 7, 8, 9, 29, 32, 3):
+    for K in (1, 2, 7, 8, 9, 16, 17, 29, 32, 33, 64, 95, 3):
         ext_h = rng.integers(0, 1 << 32, size=(K, _cabi.EXT_STRIDE), dtype=np.uint32)
         ext_h[K - 1, :1024] = 0xFFFFFFFF
         ext = torch.from_numpy(ext_h.view(np.int32)).to(dev)
