@@ -11,9 +11,9 @@
 //      K1e k_gate_bootstrap_pair  one gate per two-CTA cluster, one accumulator polynomial per SM, DSMEM
 //                                 exchange (latency path; tfhe_pair.cuh + tfhe_cluster.cuh)
 //   K2 k_key_switch       batched N -> n key switch as an integer rank-8192 update,
-//                         32 ciphertexts x 512 columns per CTA, digits in smem (launches of 33 .. 95 gates)
-//   K2n k_key_switch_narrow  the same for launches of up to 32 gates (dependent circuit levels): all loads in
-//                         flight, partial sums by atomics into a self-cleaning scratch, last CTA writes the rows
+//                         32 ciphertexts x 512 columns per CTA, digits in smem (launches of 49 .. 64 gates)
+//   K2n k_key_switch_narrow  the same for launches below 96 gates (dependent circuit levels): a batch of key loads
+//                         in flight, partial sums by atomics into a self-cleaning scratch, last CTA writes the rows
 //   K2t k_key_switch_mma  the same update as an exact s8 x u8 -> s32 GEMM on the tensor cores
 //                         (tcgen05.mma kind::i8, TMEM accumulator), tfhe_keyswitch_mma.cuh
 //   K3 k_bk_transform(_w) one-time: raw TRGSW rows -> spectral key in K1e's / K1d's chunk order;
@@ -1268,7 +1268,8 @@ static int launch_key_switch(tfb_ctx* ctx, const uint32_t* ext, void* pool, int 
     TFB_CUDA(ctx, cudaGetLastError());
     return TFB_OK;
   }
-  if (k < KSN_MAX_GATES && (ctx->force_ks == 0 || ctx->force_ks == 3)) {
+  // measured (tools/k2_ab.py): K2n wins up to 48 gates and from 65 (where K2 needs a third tile) to 95; K2 in between
+  if (k < KSN_MAX_GATES && (ctx->force_ks == 3 || (ctx->force_ks == 0 && (k <= 48 || k > 64)))) {
     const unsigned groups = (unsigned)((k + KSN_G - 1) / KSN_G);
     if (k <= KSN_SMALL_GATES)
       k_key_switch_narrow<1><<<dim3(RING_N / KSN_I, groups), KS_THREADS, 0, st>>>(
